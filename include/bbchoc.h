@@ -1,0 +1,171 @@
+/*
+ * bbchoc.h -- C ABI of the B200 (sm_100a) blocked-Bloom-with-choices hot path.
+ *
+ * This is the drop-in boundary for the reference's compiled layer
+ * (pkg/src/blowchoc/_kernels.py).  The reference's Python filter API
+ * (Filter.insert_many / contains_many / count_hits, filters.py:377-398)
+ * crosses into numba at exactly four call sites; each one maps to an entry
+ * point here:
+ *
+ *   _kernels.insert_blocks   (filters.py:383-384, _kernels.py:112-174) -> bc_insert
+ *   _kernels.contains_blocks (filters.py:394,     _kernels.py:177-211) -> bc_contains
+ *   _kernels.insert_flat     (filters.py:381,     _kernels.py:214-222) -> bc_insert
+ *   _kernels.contains_flat   (filters.py:392,     _kernels.py:225-237) -> bc_contains
+ *
+ * The numba kernels take the flat tuple built by Filter._kernel_args() and
+ * _cost_args() (filters.py:347-375) on every call.  Here that tuple is
+ * handed over once, as a bc_filter_desc, and turned into a bc_filter handle
+ * holding the derived device constants (fast-modulo magics, the cost rank
+ * table) and the scratch of the ordered insert.  Every later call takes the
+ * handle plus plain pointers and sizes.
+ *
+ * The fused DNA k-mer path replaces the composition
+ * insert_many(encode_qgrams(enc, seq)) / contains_many(encode_qgrams(enc, seq))
+ * (io.py:158-177 feeding filters.py:377-398; demos/05_dna_qgrams.py:29-52)
+ * with bc_insert_qgrams / bc_contains_qgrams, and encode_qgrams itself with
+ * bc_encode_qgrams.  bc_block_histogram replaces block_load_histogram's
+ * popcount tally (analysis.py:135-146); bc_route replaces route_many
+ * (sharding.py:50-51, filters.py:400-402).
+ *
+ * Conventions
+ *  - Return 0 on success, a negative BC_E* code on error; bc_last_error()
+ *    gives a thread-local message.  Nothing is thrown across the ABI.
+ *  - d_* pointers are device pointers (cudaMalloc / torch), h_* pointers
+ *    are host pointers (pinned or pageable).  `stream` is a cudaStream_t
+ *    (NULL = legacy default stream).  All calls are stream-ordered and do
+ *    not synchronise unless documented (the *_host entry points return
+ *    after their results are in host memory).
+ *  - Like the reference kernels, inserts require a single writer per shard;
+ *    lookups are read-only and may run concurrently.
+ */
+#ifndef BBCHOC_H
+#define BBCHOC_H
+
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define BC_API __attribute__((visibility("default")))
+#else
+#define BC_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define BC_OK 0
+#define BC_EINVAL (-1)  /* bad argument (mirrors ConfigError / ValueError) */
+#define BC_ECUDA (-2)   /* CUDA runtime error */
+#define BC_ENOMEM (-3)  /* device or pinned allocation failed */
+#define BC_EUNSUP (-4)  /* geometry outside what the kernels support */
+
+#define BC_KIND_STANDARD 0
+#define BC_KIND_BLOCKED 1
+#define BC_KIND_BLOWCHOC 2
+
+#define BC_INSERT_ORDERED 0 /* bit-identical to the reference's stream order */
+#define BC_INSERT_RELAXED 1 /* atomic OR, <= M/2 keys in flight per launch  */
+
+#define BC_MAX_CHOICES 8
+
+/* POD mirror of Filter._kernel_args() + _cost_args() (filters.py:347-375).
+ * Hash modes and shifts are NOT passed: they are a function of each range
+ * (hashing.py:65-76) and are re-derived, exactly as the reference's
+ * hash_branch does. */
+typedef struct bc_filter_desc {
+    int32_t kind;            /* BC_KIND_*                                       */
+    int32_t k;               /* bit-address functions per key                   */
+    int32_t choices;         /* c: 0 standard, 1 blocked, 2..8 blowchoc          */
+    int32_t strategy;        /* 0 random, 1 distinct                            */
+    int32_t block_bits;      /* B: multiple of 64, or 8/16/32 (toy widths)       */
+    int32_t reserved0;
+    uint64_t num_blocks;     /* M                                               */
+    uint64_t shards;         /* T (M % T == 0)                                  */
+    uint64_t shard_a;        /* h0 multiplier, range T                          */
+    uint64_t block_a[BC_MAX_CHOICES]; /* h_1..h_c multipliers, range M/T        */
+    const uint64_t *bit_a;   /* host, k multipliers                              */
+    const uint64_t *bit_b;   /* host, k ranges (B, or B-i for distinct, m for standard) */
+    int32_t cost_code;       /* 0 exp, 1 mix, 2 la (ignored for c < 2)          */
+    int32_t reserved1;
+    double cost_param;       /* beta / sigma / mu                               */
+    /* Optional host table of (B+1)*(k+1) float64 costs, cost[j*(k+1)+a].  NULL:
+     * the library evaluates the reference formulas (_kernels.py:100-109). */
+    const double *cost_table;
+} bc_filter_desc;
+
+typedef struct bc_filter bc_filter;
+
+/* Build a handle (uploads the per-filter constants to the current device). */
+BC_API int bc_filter_create(const bc_filter_desc *desc, bc_filter **out);
+BC_API void bc_filter_destroy(bc_filter *f);
+
+/* Batched insertion of n keys into d_words (num_blocks*wpb uint64 words).
+ * mode: BC_INSERT_ORDERED (exact reference semantics, any c) or
+ * BC_INSERT_RELAXED (c >= 2 only differs).  Replaces insert_blocks /
+ * insert_flat. */
+BC_API int bc_insert(bc_filter *f, uint64_t *d_words, const uint64_t *d_keys, uint64_t n,
+              int mode, void *stream);
+
+/* Batched membership.  d_out (nullable) receives 0/1 per key; d_hits
+ * (nullable) is incremented by the number of hits (count_hits).
+ * Replaces contains_blocks / contains_flat. */
+BC_API int bc_contains(bc_filter *f, const uint64_t *d_words, const uint64_t *d_keys, uint64_t n,
+                uint8_t *d_out, unsigned long long *d_hits, void *stream);
+
+/* Host-buffer variants: keys are read from, and answers written to, host
+ * memory; the library stages through its pinned buffers (or reads pinned
+ * user memory directly) and overlaps copies with the kernels.  They return
+ * once the work is complete. */
+BC_API int bc_insert_host(bc_filter *f, uint64_t *d_words, const uint64_t *h_keys, uint64_t n,
+                   int mode, void *stream);
+BC_API int bc_contains_host(bc_filter *f, const uint64_t *d_words, const uint64_t *h_keys,
+                     uint64_t n, uint8_t *h_out, unsigned long long *h_hits, void *stream);
+
+/* 2-bit canonical q-gram keys of a device byte sequence (io.py:158-177).
+ * Windows touching any byte outside ACGTacgt are skipped, so several records
+ * concatenated with a separator byte (e.g. '\n') never produce a window that
+ * spans two records.  d_keys must hold len-q+1 keys; *d_count receives the
+ * number written. */
+BC_API int bc_encode_qgrams(const uint8_t *d_seq, uint64_t len, int q, int canonical,
+                     uint64_t *d_keys, unsigned long long *d_count, void *stream);
+
+/* Fused encode + insert: == bc_insert(f, words, encode_qgrams(seq), mode).
+ * *d_count (nullable) receives the number of keys (valid windows) inserted. */
+BC_API int bc_insert_qgrams(bc_filter *f, uint64_t *d_words, const uint8_t *d_seq, uint64_t len,
+                     int q, int canonical, int mode, unsigned long long *d_count,
+                     void *stream);
+
+/* Fused encode + lookup: == bc_contains(f, words, encode_qgrams(seq)).
+ * d_out (nullable) must hold len-q+1 bytes; *d_count (nullable) receives the
+ * number of valid windows (= number of answers written). */
+BC_API int bc_contains_qgrams(bc_filter *f, const uint64_t *d_words, const uint8_t *d_seq,
+                       uint64_t len, int q, int canonical, uint8_t *d_out,
+                       unsigned long long *d_count, unsigned long long *d_hits, void *stream);
+
+/* counts[j] += number of blocks holding j set bits, j in [0, block_bits]. */
+BC_API int bc_block_histogram(const uint64_t *d_words, uint64_t num_blocks, int block_bits,
+                       unsigned long long *d_counts, void *stream);
+
+/* Shard index h0(x) per key (route_many). */
+BC_API int bc_route(bc_filter *f, const uint64_t *d_keys, uint64_t n, uint64_t *d_shard,
+             void *stream);
+
+/* Generic ((a*x mod 2^64) folded) mod b over a key array (eval_hash_many,
+ * hashing.py:90-100). */
+BC_API int bc_eval_hash(uint64_t a, uint64_t b, const uint64_t *d_keys, uint64_t n,
+                 uint64_t *d_out, void *stream);
+
+/* Thread-local description of the last error on this thread. */
+BC_API const char *bc_last_error(void);
+
+/* Number of kernels this library has launched (process-wide counter). */
+BC_API unsigned long long bc_launch_count(void);
+
+/* Library version string. */
+BC_API const char *bc_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* BBCHOC_H */

@@ -1,0 +1,633 @@
+// C ABI (include/bbchoc.h): filter handles, argument validation, dispatch to
+// the kernels, host-buffer staging.  No exception crosses this boundary.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/bbchoc.h"
+#include "launch.h"
+
+using namespace bc;
+
+namespace bc {
+unsigned long long launch_count();
+}
+
+// ---------------------------------------------------------------------------------
+static thread_local std::string g_err;
+
+static int fail(int code, const char *fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return code;
+}
+
+#define CUDA_TRY(expr)                                                                   \
+    do {                                                                                 \
+        cudaError_t e__ = (expr);                                                        \
+        if (e__ != cudaSuccess)                                                          \
+            return fail(e__ == cudaErrorMemoryAllocation ? BC_ENOMEM : BC_ECUDA,         \
+                        "%s: %s (%s:%d)", #expr, cudaGetErrorString(e__), __FILE__,      \
+                        __LINE__);                                                       \
+    } while (0)
+
+static DevHash make_dev_hash(u64 a, u64 b) {
+    DevHash h;
+    h.a = a;
+    h.b = b;
+    h.magic = 0;
+    h.shift = 0;
+    if (b == 1) {
+        h.mode = ZERO;  // MOD_ODD with b = 1: always 0
+    } else if (b & 1) {
+        h.mode = MOD_ODD;
+    } else if ((b & (b - 1)) == 0) {
+        h.mode = SHIFT_POW2;
+        h.shift = 64 - (63 - __builtin_clzll(b));  // hashing.py:73-74
+    } else {
+        h.mode = XOR_EVEN;
+        h.shift = 32;  // u // 2, hashing.py:76
+    }
+    if (h.mode == MOD_ODD || h.mode == XOR_EVEN)
+        h.magic = (u64)(((unsigned __int128)1 << 64) / b);
+    return h;
+}
+
+// Reference cost formulas, evaluated in the same operation order as
+// _kernels.py:100-109 (IEEE double, no contraction: see the build flags).
+static double ref_cost(int code, double param, int j, int a, int k, int block_bits) {
+    const double jf = (double)j, af = (double)a, kf = (double)k;
+    const double quarter = block_bits / 4.0, half = block_bits / 2.0;
+    if (code == 0) return std::pow(param, jf / quarter) + af / kf;
+    if (code == 1) return param * kf * std::pow(jf / half, kf) + af;
+    return kf * std::pow((jf + param * kf) / half, kf) + af;
+}
+
+struct bc_filter {
+    int device = 0;
+    int kind = 0;
+    KParams kp{};
+    DevHash *d_bits = nullptr;
+    u32 *d_rank = nullptr;
+    std::mutex mu;  // ordered-insert scratch
+    u64 *d_owner = nullptr;
+    u32 *d_lists = nullptr;
+    u32 *d_state = nullptr;
+    u64 chunk = 0;
+    u64 rounds_bound = 0;
+};
+
+// ---------------------------------------------------------------------------------
+extern "C" const char *bc_last_error(void) { return g_err.c_str(); }
+
+extern "C" unsigned long long bc_launch_count(void) { return bc::launch_count(); }
+
+extern "C" const char *bc_version(void) { return "bbchoc-b200 0.1.0 (sm_100a)"; }
+
+extern "C" int bc_filter_create(const bc_filter_desc *d, bc_filter **out) {
+    if (!d || !out) return fail(BC_EINVAL, "null argument");
+    *out = nullptr;
+    const int B = d->block_bits;
+    const bool toy = (B == 8 || B == 16 || B == 32);
+    if (!(toy || (B > 0 && B % 64 == 0))) return fail(BC_EINVAL, "invalid block_bits %d", B);
+    if (d->kind < 0 || d->kind > 2) return fail(BC_EINVAL, "unknown kind %d", d->kind);
+    if (d->k < 1 || d->k > B) return fail(BC_EINVAL, "k must be in [1, %d], got %d", B, d->k);
+    if (d->strategy != 0 && d->strategy != 1)
+        return fail(BC_EINVAL, "unknown strategy %d", d->strategy);
+    if (d->num_blocks < 1 || d->shards < 1 || d->num_blocks % d->shards != 0)
+        return fail(BC_EINVAL, "%llu blocks do not split into %llu shards",
+                    (unsigned long long)d->num_blocks, (unsigned long long)d->shards);
+    if (!d->bit_a || !d->bit_b) return fail(BC_EINVAL, "bit_a / bit_b must be given");
+    const int c = d->choices;
+    if (d->kind == BC_KIND_STANDARD) {
+        if (c != 0) return fail(BC_EINVAL, "standard filters have 0 choices");
+        if (d->strategy != 0 || d->shards != 1 || toy)
+            return fail(BC_EINVAL, "standard filters are random, unsharded, word-multiple");
+    } else if (d->kind == BC_KIND_BLOCKED) {
+        if (c != 1) return fail(BC_EINVAL, "blocked filters have exactly one choice");
+    } else if (c < 2 || c > BC_MAX_CHOICES) {
+        return fail(BC_EINVAL, "blowchoc needs between 2 and %d choices, got %d",
+                    BC_MAX_CHOICES, c);
+    }
+    const int wpb = B >= 64 ? B / 64 : 1;
+    if (d->kind != BC_KIND_STANDARD && wpb > kMaxWpb)
+        return fail(BC_EUNSUP, "block_bits %d above the supported %d", B, kMaxWpb * 64);
+    if (d->kind != BC_KIND_STANDARD && d->num_blocks >= (1ull << 32))
+        return fail(BC_EUNSUP, "more than 2^32 blocks");
+    for (int i = 0; i < d->k; ++i)
+        if (d->bit_b[i] < 1) return fail(BC_EINVAL, "bit range %d is zero", i);
+
+    bc_filter *f = new (std::nothrow) bc_filter();
+    if (!f) return fail(BC_ENOMEM, "out of host memory");
+    cudaGetDevice(&f->device);
+    f->kind = d->kind;
+    KParams &p = f->kp;
+    p.k = (u32)d->k;
+    p.c = (u32)(d->kind == BC_KIND_STANDARD ? 0 : c);
+    p.wpb = (u32)wpb;
+    p.strategy = (u32)d->strategy;
+    p.block_bits = (u32)B;
+    p.num_blocks = d->num_blocks;
+    p.per_shard = d->num_blocks / d->shards;
+    p.shard = make_dev_hash(d->shard_a, d->shards);
+    p.block = make_dev_hash(0, p.per_shard);
+    for (int ci = 0; ci < BC_MAX_CHOICES; ++ci) p.block_a[ci] = ci < c ? d->block_a[ci] : 0;
+    if (d->kind == BC_KIND_STANDARD) {
+        const u64 m = d->num_blocks * (u64)B;
+        DevHash fh = make_dev_hash(0, m);
+        p.flat_b = m;
+        p.flat_magic = fh.magic;
+        p.flat_mode = fh.mode;
+        p.flat_shift = fh.shift;
+    }
+    std::vector<DevHash> bits(d->k);
+    bool fast = d->kind != BC_KIND_STANDARD && d->strategy == 0 && B == 512 && d->k <= kMaxFastK;
+    for (int i = 0; i < d->k; ++i) {
+        bits[i] = make_dev_hash(d->bit_a[i], d->bit_b[i]);
+        if (d->bit_b[i] != 512) fast = false;
+        if (i < kMaxFastK) {
+            p.bit_a_lo[i] = (u32)d->bit_a[i];
+            p.bit_a_hi[i] = (u32)(d->bit_a[i] >> 32);
+        }
+    }
+    p.fast_random = fast ? 1u : 0u;
+
+    auto cleanup = [&](int rc) {
+        bc_filter_destroy(f);
+        return rc;
+    };
+    cudaError_t e = cudaMalloc(&f->d_bits, sizeof(DevHash) * bits.size());
+    if (e != cudaSuccess) return cleanup(fail(BC_ENOMEM, "cudaMalloc: %s", cudaGetErrorString(e)));
+    e = cudaMemcpy(f->d_bits, bits.data(), sizeof(DevHash) * bits.size(), cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) return cleanup(fail(BC_ECUDA, "cudaMemcpy: %s", cudaGetErrorString(e)));
+    p.bits = f->d_bits;
+
+    if (c >= 2) {
+        // Dense ranks of the float64 costs: cost_i < cost_j  <=>  rank_i < rank_j,
+        // equal costs share a rank; +inf and NaN never beat the initial +inf
+        // (_kernels.py:156-170), so they get the sentinel rank.
+        const int K1 = d->k + 1;
+        const size_t cells = (size_t)(B + 1) * K1;
+        std::vector<double> cost(cells);
+        for (int j = 0; j <= B; ++j)
+            for (int a = 0; a <= d->k; ++a)
+                cost[(size_t)j * K1 + a] = d->cost_table
+                                               ? d->cost_table[(size_t)j * K1 + a]
+                                               : ref_cost(d->cost_code, d->cost_param, j, a,
+                                                          d->k, B);
+        std::vector<double> uniq;
+        uniq.reserve(cells);
+        for (double v : cost)
+            if (!std::isnan(v) && !(std::isinf(v) && v > 0)) uniq.push_back(v);
+        std::sort(uniq.begin(), uniq.end());
+        uniq.erase(std::unique(uniq.begin(), uniq.end()), uniq.end());
+        std::vector<u32> rank(cells);
+        for (size_t i = 0; i < cells; ++i) {
+            const double v = cost[i];
+            if (std::isnan(v) || (std::isinf(v) && v > 0))
+                rank[i] = 0xffffffffu;
+            else
+                rank[i] = (u32)(std::lower_bound(uniq.begin(), uniq.end(), v) - uniq.begin());
+        }
+        e = cudaMalloc(&f->d_rank, sizeof(u32) * cells);
+        if (e != cudaSuccess)
+            return cleanup(fail(BC_ENOMEM, "cudaMalloc: %s", cudaGetErrorString(e)));
+        e = cudaMemcpy(f->d_rank, rank.data(), sizeof(u32) * cells, cudaMemcpyHostToDevice);
+        if (e != cudaSuccess)
+            return cleanup(fail(BC_ECUDA, "cudaMemcpy: %s", cudaGetErrorString(e)));
+    }
+    p.rank = f->d_rank;
+    *out = f;
+    return BC_OK;
+}
+
+extern "C" void bc_filter_destroy(bc_filter *f) {
+    if (!f) return;
+    int prev = 0;
+    cudaGetDevice(&prev);
+    cudaSetDevice(f->device);
+    cudaFree(f->d_bits);
+    cudaFree(f->d_rank);
+    cudaFree(f->d_owner);
+    cudaFree(f->d_lists);
+    cudaFree(f->d_state);
+    cudaSetDevice(prev);
+    delete f;
+}
+
+static int check_device(bc_filter *f) {
+    int dev = -1;
+    cudaGetDevice(&dev);
+    if (dev != f->device)
+        return fail(BC_EINVAL, "filter handle belongs to device %d, current device is %d",
+                    f->device, dev);
+    return BC_OK;
+}
+
+// Ordered-insert scratch: owner[M] (u64), two pending lists of `chunk` u32,
+// state = {round, counter0, counter1}.
+static int ensure_ordered_scratch(bc_filter *f, cudaStream_t s) {
+    if (f->d_owner) return BC_OK;
+    const u64 M = f->kp.num_blocks;
+    u64 chunk = M / 8;
+    chunk = std::max<u64>(chunk, 256);
+    chunk = std::min<u64>(chunk, 1ull << 24);
+    CUDA_TRY(cudaMalloc(&f->d_owner, sizeof(u64) * M));
+    CUDA_TRY(cudaMalloc(&f->d_lists, sizeof(u32) * 2 * chunk));
+    CUDA_TRY(cudaMalloc(&f->d_state, sizeof(u32) * 4));
+    CUDA_TRY(cudaMemsetAsync(f->d_owner, 0xff, sizeof(u64) * M, s));
+    CUDA_TRY(cudaMemsetAsync(f->d_state, 0, sizeof(u32) * 4, s));
+    f->chunk = chunk;
+    f->rounds_bound = 0;
+    return BC_OK;
+}
+
+static int insert_device(bc_filter *f, u64 *words, const u64 *keys, u64 n, int mode,
+                         cudaStream_t s) {
+    if (n == 0) return BC_OK;
+    if (f->kind == BC_KIND_STANDARD) {
+        CUDA_TRY(launch_flat(OP_INSERT, f->kp, words, keys, n, nullptr, nullptr, s));
+        return BC_OK;
+    }
+    if (f->kp.c == 1) {  // OR commutes: any order is the reference's order
+        CUDA_TRY(launch_blocks(OP_INSERT, f->kp, words, keys, n, nullptr, nullptr, s));
+        return BC_OK;
+    }
+    if (mode == BC_INSERT_RELAXED) {
+        // keep at most M/2 keys in flight (FPR within ~3%)
+        const u64 per = std::max<u64>(1, f->kp.num_blocks / 2);
+        for (u64 off = 0; off < n; off += per)
+            CUDA_TRY(launch_blocks(OP_INSERT, f->kp, words, keys + off, std::min(per, n - off),
+                                   nullptr, nullptr, s));
+        return BC_OK;
+    }
+    std::lock_guard<std::mutex> lk(f->mu);
+    int rc = ensure_ordered_scratch(f, s);
+    if (rc) return rc;
+    // every round commits at least one key, so rounds <= keys: re-arm the
+    // round tags long before the 32-bit counter could wrap
+    if (f->rounds_bound + n >= (1ull << 31)) {
+        CUDA_TRY(cudaMemsetAsync(f->d_owner, 0xff, sizeof(u64) * f->kp.num_blocks, s));
+        CUDA_TRY(cudaMemsetAsync(f->d_state, 0, sizeof(u32) * 4, s));
+        f->rounds_bound = 0;
+    }
+    for (u64 off = 0; off < n; off += (1ull << 30)) {
+        const u64 len = std::min<u64>(1ull << 30, n - off);
+        CUDA_TRY(launch_ordered(f->kp, words, keys + off, len, f->chunk, f->d_owner, f->d_lists,
+                                f->d_state, s));
+        f->rounds_bound += len;
+    }
+    return BC_OK;
+}
+
+extern "C" int bc_insert(bc_filter *f, uint64_t *d_words, const uint64_t *d_keys, uint64_t n,
+                         int mode, void *stream) {
+    if (!f) return fail(BC_EINVAL, "null filter");
+    if (n && (!d_words || !d_keys)) return fail(BC_EINVAL, "null words or keys");
+    if (mode != BC_INSERT_ORDERED && mode != BC_INSERT_RELAXED)
+        return fail(BC_EINVAL, "unknown insert mode %d", mode);
+    if (int rc = check_device(f)) return rc;
+    return insert_device(f, d_words, d_keys, n, mode, (cudaStream_t)stream);
+}
+
+static int contains_device(bc_filter *f, const u64 *words, const u64 *keys, u64 n, u8 *out,
+                           unsigned long long *hits, cudaStream_t s) {
+    if (n == 0) return BC_OK;
+    if (f->kind == BC_KIND_STANDARD)
+        CUDA_TRY(launch_flat(OP_CONTAINS, f->kp, const_cast<u64 *>(words), keys, n, out, hits, s));
+    else
+        CUDA_TRY(launch_blocks(OP_CONTAINS, f->kp, const_cast<u64 *>(words), keys, n, out, hits,
+                               s));
+    return BC_OK;
+}
+
+extern "C" int bc_contains(bc_filter *f, const uint64_t *d_words, const uint64_t *d_keys,
+                           uint64_t n, uint8_t *d_out, unsigned long long *d_hits, void *stream) {
+    if (!f) return fail(BC_EINVAL, "null filter");
+    if (n && (!d_words || !d_keys)) return fail(BC_EINVAL, "null words or keys");
+    if (int rc = check_device(f)) return rc;
+    return contains_device(f, d_words, d_keys, n, d_out, d_hits, (cudaStream_t)stream);
+}
+
+// ---- q-grams ------------------------------------------------------------------------
+static u64 qgram_windows(u64 len, int q) { return len >= (u64)q ? len - (u64)q + 1 : 0; }
+
+extern "C" int bc_encode_qgrams(const uint8_t *d_seq, uint64_t len, int q, int canonical,
+                                uint64_t *d_keys, unsigned long long *d_count, void *stream) {
+    if (q < 1 || q > 32) return fail(BC_EINVAL, "q must be in [1, 32], got %d", q);
+    cudaStream_t s = (cudaStream_t)stream;
+    const u64 nwin = qgram_windows(len, q);
+    if (nwin == 0) {
+        if (d_count) CUDA_TRY(cudaMemsetAsync(d_count, 0, sizeof(*d_count), s));
+        return BC_OK;
+    }
+    if (!d_seq || !d_keys) return fail(BC_EINVAL, "null sequence or key buffer");
+    const u64 ntiles = (nwin + kQgramTile - 1) / kQgramTile;
+    u64 *tiles = nullptr;
+    CUDA_TRY(cudaMallocAsync((void **)&tiles, sizeof(u64) * ntiles, s));
+    cudaError_t e = launch_qgram_offsets(d_seq, len, q, tiles, ntiles, d_count, s);
+    if (e == cudaSuccess) e = launch_qgram_encode(d_seq, len, q, canonical, tiles, d_keys, s);
+    cudaFreeAsync(tiles, s);
+    CUDA_TRY(e);
+    return BC_OK;
+}
+
+// Materialise the keys (for the paths the fused kernel does not cover:
+// ordered c >= 2 inserts, standard filters, non-512-bit blocks).
+static int encode_tmp(const u8 *seq, u64 len, int q, int canonical, u64 **keys, u64 *n,
+                      cudaStream_t s) {
+    const u64 nwin = qgram_windows(len, q);
+    *keys = nullptr;
+    *n = 0;
+    if (nwin == 0) return BC_OK;
+    unsigned long long *d_cnt = nullptr;
+    CUDA_TRY(cudaMallocAsync((void **)keys, sizeof(u64) * nwin, s));
+    CUDA_TRY(cudaMallocAsync((void **)&d_cnt, sizeof(*d_cnt), s));
+    int rc = bc_encode_qgrams(seq, len, q, canonical, *keys, d_cnt, s);
+    unsigned long long h_cnt = 0;
+    if (rc == BC_OK) {
+        cudaError_t e = cudaMemcpyAsync(&h_cnt, d_cnt, sizeof h_cnt, cudaMemcpyDeviceToHost, s);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+        if (e != cudaSuccess) rc = fail(BC_ECUDA, "%s", cudaGetErrorString(e));
+    }
+    cudaFreeAsync(d_cnt, s);
+    *n = h_cnt;
+    return rc;
+}
+
+extern "C" int bc_insert_qgrams(bc_filter *f, uint64_t *d_words, const uint8_t *d_seq,
+                                uint64_t len, int q, int canonical, int mode,
+                                unsigned long long *d_count, void *stream) {
+    if (!f) return fail(BC_EINVAL, "null filter");
+    if (q < 1 || q > 32) return fail(BC_EINVAL, "q must be in [1, 32], got %d", q);
+    if (mode != BC_INSERT_ORDERED && mode != BC_INSERT_RELAXED)
+        return fail(BC_EINVAL, "unknown insert mode %d", mode);
+    if (int rc = check_device(f)) return rc;
+    cudaStream_t s = (cudaStream_t)stream;
+    const u64 nwin = qgram_windows(len, q);
+    if (d_count) CUDA_TRY(cudaMemsetAsync(d_count, 0, sizeof(*d_count), s));
+    if (nwin == 0) return BC_OK;
+    if (!d_words || !d_seq) return fail(BC_EINVAL, "null words or sequence");
+    const bool fused = f->kind != BC_KIND_STANDARD && f->kp.wpb == 8 &&
+                       (f->kp.c == 1 || mode == BC_INSERT_RELAXED);
+    if (fused) {
+        // c == 1: one launch.  relaxed: windows in slices of M/2.
+        const u64 per = f->kp.c == 1 ? nwin : std::max<u64>(1, f->kp.num_blocks / 2);
+        for (u64 w = 0; w < nwin; w += per) {
+            const u64 nw = std::min(per, nwin - w);
+            CUDA_TRY(launch_qgram_blocks(OP_INSERT, f->kp, d_words, d_seq + w, nw + q - 1, q,
+                                         canonical, nullptr, nullptr, nullptr, d_count, s));
+        }
+        return BC_OK;
+    }
+    u64 *keys = nullptr, n = 0;
+    int rc = encode_tmp(d_seq, len, q, canonical, &keys, &n, s);
+    if (rc == BC_OK) rc = insert_device(f, d_words, keys, n, mode, s);
+    if (rc == BC_OK && d_count) {
+        unsigned long long hn = n;
+        cudaError_t e = cudaMemcpyAsync(d_count, &hn, sizeof hn, cudaMemcpyHostToDevice, s);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+        if (e != cudaSuccess) rc = fail(BC_ECUDA, "%s", cudaGetErrorString(e));
+    }
+    if (keys) cudaFreeAsync(keys, s);
+    return rc;
+}
+
+extern "C" int bc_contains_qgrams(bc_filter *f, const uint64_t *d_words, const uint8_t *d_seq,
+                                  uint64_t len, int q, int canonical, uint8_t *d_out,
+                                  unsigned long long *d_count, unsigned long long *d_hits,
+                                  void *stream) {
+    if (!f) return fail(BC_EINVAL, "null filter");
+    if (q < 1 || q > 32) return fail(BC_EINVAL, "q must be in [1, 32], got %d", q);
+    if (int rc = check_device(f)) return rc;
+    cudaStream_t s = (cudaStream_t)stream;
+    const u64 nwin = qgram_windows(len, q);
+    if (nwin == 0) {
+        if (d_count) CUDA_TRY(cudaMemsetAsync(d_count, 0, sizeof(*d_count), s));
+        return BC_OK;
+    }
+    if (!d_words || !d_seq) return fail(BC_EINVAL, "null words or sequence");
+    if (f->kind != BC_KIND_STANDARD && f->kp.wpb == 8) {
+        const u64 ntiles = (nwin + kQgramTile - 1) / kQgramTile;
+        u64 *tiles = nullptr;
+        const bool need_off = d_out != nullptr || d_count != nullptr;
+        if (need_off) {
+            CUDA_TRY(cudaMallocAsync((void **)&tiles, sizeof(u64) * ntiles, s));
+            cudaError_t e = launch_qgram_offsets(d_seq, len, q, tiles, ntiles, d_count, s);
+            if (e != cudaSuccess) {
+                cudaFreeAsync(tiles, s);
+                CUDA_TRY(e);
+            }
+        }
+        cudaError_t e = launch_qgram_blocks(OP_CONTAINS, f->kp, const_cast<u64 *>(d_words), d_seq,
+                                            len, q, canonical, tiles, d_out, d_hits, nullptr, s);
+        if (tiles) cudaFreeAsync(tiles, s);
+        CUDA_TRY(e);
+        return BC_OK;
+    }
+    u64 *keys = nullptr, n = 0;
+    int rc = encode_tmp(d_seq, len, q, canonical, &keys, &n, s);
+    if (rc == BC_OK) rc = contains_device(f, d_words, keys, n, d_out, d_hits, s);
+    if (rc == BC_OK && d_count) {
+        unsigned long long hn = n;
+        cudaError_t e = cudaMemcpyAsync(d_count, &hn, sizeof hn, cudaMemcpyHostToDevice, s);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+        if (e != cudaSuccess) rc = fail(BC_ECUDA, "%s", cudaGetErrorString(e));
+    }
+    if (keys) cudaFreeAsync(keys, s);
+    return rc;
+}
+
+// ---- analysis / routing ---------------------------------------------------------------
+extern "C" int bc_block_histogram(const uint64_t *d_words, uint64_t num_blocks, int block_bits,
+                                  unsigned long long *d_counts, void *stream) {
+    const bool toy = (block_bits == 8 || block_bits == 16 || block_bits == 32);
+    if (!(toy || (block_bits > 0 && block_bits % 64 == 0)))
+        return fail(BC_EINVAL, "invalid block_bits %d", block_bits);
+    if (num_blocks && (!d_words || !d_counts)) return fail(BC_EINVAL, "null words or counts");
+    CUDA_TRY(launch_histogram(d_words, num_blocks, block_bits, d_counts, (cudaStream_t)stream));
+    return BC_OK;
+}
+
+extern "C" int bc_route(bc_filter *f, const uint64_t *d_keys, uint64_t n, uint64_t *d_shard,
+                        void *stream) {
+    if (!f) return fail(BC_EINVAL, "null filter");
+    if (n && (!d_keys || !d_shard)) return fail(BC_EINVAL, "null keys or output");
+    if (int rc = check_device(f)) return rc;
+    CUDA_TRY(launch_eval_hash(f->kp.shard, d_keys, n, d_shard, (cudaStream_t)stream));
+    return BC_OK;
+}
+
+extern "C" int bc_eval_hash(uint64_t a, uint64_t b, const uint64_t *d_keys, uint64_t n,
+                            uint64_t *d_out, void *stream) {
+    if (b < 1) return fail(BC_EINVAL, "hash range must be >= 1, got %llu", (unsigned long long)b);
+    if (n && (!d_keys || !d_out)) return fail(BC_EINVAL, "null keys or output");
+    CUDA_TRY(launch_eval_hash(make_dev_hash(a, b), d_keys, n, d_out, (cudaStream_t)stream));
+    return BC_OK;
+}
+
+// ---- host-buffer entry points ---------------------------------------------------------
+// Per-device staging: two pinned key buffers, two pinned answer buffers, two
+// device key/answer buffers and two copy streams, so the copy of chunk i+1
+// (and the answers of chunk i-1) overlap the kernel of chunk i, while the
+// kernels themselves run in order on the caller's stream.
+namespace {
+constexpr u64 kStageKeys = 1ull << 22;  // 32 MiB of keys per buffer
+
+struct Staging {
+    std::mutex mu;
+    bool ready = false;
+    u64 *h_keys[2] = {nullptr, nullptr};
+    u8 *h_out[2] = {nullptr, nullptr};
+    u64 *d_keys[2] = {nullptr, nullptr};
+    u8 *d_out[2] = {nullptr, nullptr};
+    cudaStream_t cs[2] = {nullptr, nullptr};
+    cudaEvent_t h2d[2], kdone[2], done[2];
+};
+
+std::mutex g_stage_mu;
+std::map<int, Staging *> g_stage;
+
+Staging *staging_for(int dev) {
+    std::lock_guard<std::mutex> lk(g_stage_mu);
+    auto it = g_stage.find(dev);
+    if (it != g_stage.end()) return it->second;
+    Staging *st = new Staging();
+    g_stage[dev] = st;
+    return st;
+}
+
+int staging_init(Staging *st) {
+    if (st->ready) return BC_OK;
+    for (int b = 0; b < 2; ++b) {
+        CUDA_TRY(cudaHostAlloc((void **)&st->h_keys[b], sizeof(u64) * kStageKeys,
+                               cudaHostAllocDefault));
+        CUDA_TRY(cudaHostAlloc((void **)&st->h_out[b], kStageKeys, cudaHostAllocDefault));
+        CUDA_TRY(cudaMalloc((void **)&st->d_keys[b], sizeof(u64) * kStageKeys));
+        CUDA_TRY(cudaMalloc((void **)&st->d_out[b], kStageKeys));
+        CUDA_TRY(cudaStreamCreateWithFlags(&st->cs[b], cudaStreamNonBlocking));
+        CUDA_TRY(cudaEventCreateWithFlags(&st->h2d[b], cudaEventDisableTiming));
+        CUDA_TRY(cudaEventCreateWithFlags(&st->kdone[b], cudaEventDisableTiming));
+        CUDA_TRY(cudaEventCreateWithFlags(&st->done[b], cudaEventDisableTiming));
+        CUDA_TRY(cudaEventRecord(st->done[b], st->cs[b]));
+    }
+    st->ready = true;
+    return BC_OK;
+}
+
+bool is_pinned(const void *p) {
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeHost;
+}
+}  // namespace
+
+static int host_pipeline(bc_filter *f, u64 *words, const u64 *h_keys, u64 n, int op, int mode,
+                         u8 *h_out, unsigned long long *h_hits, cudaStream_t s) {
+    Staging *st = staging_for(f->device);
+    std::lock_guard<std::mutex> lk(st->mu);
+    if (int rc = staging_init(st)) return rc;
+    const bool keys_pinned = is_pinned(h_keys);
+    const bool out_pinned = h_out != nullptr && is_pinned(h_out);
+    unsigned long long *d_hits = nullptr;
+    if (h_hits) {
+        CUDA_TRY(cudaMallocAsync((void **)&d_hits, sizeof(*d_hits), s));
+        CUDA_TRY(cudaMemsetAsync(d_hits, 0, sizeof(*d_hits), s));
+    }
+    // the copy streams must not start before earlier work on `s`
+    cudaEvent_t start;
+    CUDA_TRY(cudaEventCreateWithFlags(&start, cudaEventDisableTiming));
+    CUDA_TRY(cudaEventRecord(start, s));
+    for (int b = 0; b < 2; ++b) CUDA_TRY(cudaStreamWaitEvent(st->cs[b], start, 0));
+
+    struct Pending {
+        u64 off = 0, len = 0;
+        bool live = false;
+    } pend[2];
+    int rc = BC_OK;
+    u64 chunk_i = 0;
+    for (u64 off = 0; off < n && rc == BC_OK; off += kStageKeys, ++chunk_i) {
+        const int b = (int)(chunk_i & 1);
+        const u64 len = std::min(kStageKeys, n - off);
+        CUDA_TRY(cudaEventSynchronize(st->done[b]));  // buffer b is free again
+        if (pend[b].live && h_out && !out_pinned)
+            std::memcpy(h_out + pend[b].off, st->h_out[b], pend[b].len);
+        pend[b].live = false;
+        const u64 *src = h_keys + off;
+        if (!keys_pinned) {
+            std::memcpy(st->h_keys[b], src, sizeof(u64) * len);
+            src = st->h_keys[b];
+        }
+        CUDA_TRY(cudaMemcpyAsync(st->d_keys[b], src, sizeof(u64) * len, cudaMemcpyHostToDevice,
+                                 st->cs[b]));
+        CUDA_TRY(cudaEventRecord(st->h2d[b], st->cs[b]));
+        CUDA_TRY(cudaStreamWaitEvent(s, st->h2d[b], 0));
+        if (op == OP_INSERT)
+            rc = insert_device(f, words, st->d_keys[b], len, mode, s);
+        else
+            rc = contains_device(f, words, st->d_keys[b], len, h_out ? st->d_out[b] : nullptr,
+                                 d_hits, s);
+        if (rc) break;
+        CUDA_TRY(cudaEventRecord(st->kdone[b], s));
+        CUDA_TRY(cudaStreamWaitEvent(st->cs[b], st->kdone[b], 0));
+        if (h_out) {
+            u8 *dst = out_pinned ? h_out + off : st->h_out[b];
+            CUDA_TRY(cudaMemcpyAsync(dst, st->d_out[b], len, cudaMemcpyDeviceToHost, st->cs[b]));
+            pend[b] = {off, len, true};
+        }
+        CUDA_TRY(cudaEventRecord(st->done[b], st->cs[b]));
+    }
+    for (int b = 0; b < 2; ++b) {
+        CUDA_TRY(cudaEventSynchronize(st->done[b]));
+        if (pend[b].live && h_out && !out_pinned)
+            std::memcpy(h_out + pend[b].off, st->h_out[b], pend[b].len);
+    }
+    if (d_hits) {
+        unsigned long long v = 0;
+        CUDA_TRY(cudaMemcpyAsync(&v, d_hits, sizeof v, cudaMemcpyDeviceToHost, s));
+        CUDA_TRY(cudaFreeAsync(d_hits, s));
+        CUDA_TRY(cudaStreamSynchronize(s));
+        *h_hits += v;
+    }
+    CUDA_TRY(cudaStreamSynchronize(s));
+    cudaEventDestroy(start);
+    return rc;
+}
+
+extern "C" int bc_insert_host(bc_filter *f, uint64_t *d_words, const uint64_t *h_keys,
+                              uint64_t n, int mode, void *stream) {
+    if (!f) return fail(BC_EINVAL, "null filter");
+    if (n && (!d_words || !h_keys)) return fail(BC_EINVAL, "null words or keys");
+    if (mode != BC_INSERT_ORDERED && mode != BC_INSERT_RELAXED)
+        return fail(BC_EINVAL, "unknown insert mode %d", mode);
+    if (int rc = check_device(f)) return rc;
+    if (n == 0) return BC_OK;
+    return host_pipeline(f, d_words, h_keys, n, OP_INSERT, mode, nullptr, nullptr,
+                         (cudaStream_t)stream);
+}
+
+extern "C" int bc_contains_host(bc_filter *f, const uint64_t *d_words, const uint64_t *h_keys,
+                                uint64_t n, uint8_t *h_out, unsigned long long *h_hits,
+                                void *stream) {
+    if (!f) return fail(BC_EINVAL, "null filter");
+    if (n && (!d_words || !h_keys)) return fail(BC_EINVAL, "null words or keys");
+    if (int rc = check_device(f)) return rc;
+    if (n == 0) return BC_OK;
+    return host_pipeline(f, const_cast<u64 *>(d_words), h_keys, n, OP_CONTAINS, 0, h_out,
+                         h_hits, (cudaStream_t)stream);
+}

@@ -1,0 +1,352 @@
+// Kernels of the blocked / blowchoc / standard filter hot path.
+//
+//   blocks512_kernel<OP, C>  key array -> lookup answers or inserts, 512-bit
+//                            blocks, two-phase tile (blocks.cuh)
+//   generic_kernel<OP>       thread per key, any block width (toy 8/16/32,
+//                            64..4096 bits)
+//   ordered_kernel           exact stream-order insert for c >= 2: claim
+//                            rounds inside one cooperative launch
+//   flat_kernel<OP>          standard Bloom filter (k global bits)
+//   hist512_kernel / hist_generic_kernel   per-block popcount tally
+//   eval_hash_kernel         one hash over a key array (routing)
+#include <cooperative_groups.h>
+
+#include <atomic>
+#include <mutex>
+#include <unordered_map>
+
+#include "blocks.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace bc {
+
+static std::atomic<unsigned long long> g_launches{0};
+
+void count_launch(unsigned n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+
+unsigned long long launch_count() { return g_launches.load(std::memory_order_relaxed); }
+
+static int sm_count() {
+    int dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    return sms > 0 ? sms : 1;
+}
+
+unsigned grid_for(const void *kernel, int threads, size_t dyn_smem,
+                  unsigned long long work_ctas) {
+    static std::mutex mu;
+    static std::unordered_map<const void *, int> occ;
+    int per_sm = 0;
+    {
+        std::lock_guard<std::mutex> lk(mu);
+        auto it = occ.find(kernel);
+        if (it == occ.end()) {
+            if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads,
+                                                              dyn_smem) != cudaSuccess ||
+                per_sm < 1)
+                per_sm = 1;
+            occ[kernel] = per_sm;
+        } else {
+            per_sm = it->second;
+        }
+    }
+    unsigned long long cap = (unsigned long long)per_sm * (unsigned long long)sm_count();
+    if (work_ctas < 1) work_ctas = 1;
+    return (unsigned)(work_ctas < cap ? work_ctas : cap);
+}
+
+// ---------------------------------------------------------------------------------
+template <int OP, int C>
+__global__ void __launch_bounds__(kTPB) blocks512_kernel(const __grid_constant__ KParams p,
+                                                         u64 *__restrict__ words,
+                                                         const u64 *__restrict__ keys, u64 n,
+                                                         u8 *__restrict__ out,
+                                                         unsigned long long *__restrict__ hits) {
+    __shared__ TileSmem<C> sm;
+    const int tid = threadIdx.x;
+    const u64 ntiles = (n + kTPB - 1) / kTPB;
+    u32 my_hits = 0;
+    for (u64 tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const u64 base = tile * kTPB;
+        const u32 cnt = (u32)min((u64)kTPB, n - base);
+        const bool valid = (u32)tid < cnt;
+        const u64 x = valid ? ld_stream(keys + base + tid) : 0ull;
+        phase1<C>(p, x, valid, sm, tid);
+        __syncthreads();
+        my_hits += phase2<OP, C>(p, words, sm, cnt, tid);
+        __syncthreads();
+        if (OP == OP_CONTAINS && out != nullptr && valid) out[base + tid] = sm.out[tid];
+    }
+    if (OP == OP_CONTAINS && hits != nullptr) {
+        for (int o = 16; o > 0; o >>= 1) my_hits += __shfl_xor_sync(kFull, my_hits, o);
+        if ((tid & 31) == 0 && my_hits) atomicAdd(hits, (unsigned long long)my_hits);
+    }
+}
+
+template <int OP>
+__global__ void __launch_bounds__(256) generic_kernel(const __grid_constant__ KParams p,
+                                                      u64 *__restrict__ words,
+                                                      const u64 *__restrict__ keys, u64 n,
+                                                      u8 *__restrict__ out,
+                                                      unsigned long long *__restrict__ hits) {
+    u64 mask[kMaxWpb];
+    u32 my_hits = 0;
+    const u64 stride = (u64)gridDim.x * blockDim.x;
+    for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < n; i += stride) {
+        const u64 x = ld_stream(keys + i);
+        build_mask_generic(p, x, mask);
+        if (OP == OP_CONTAINS) {
+            bool found = false;
+            for (u32 ci = 0; ci < p.c && !found; ++ci) {
+                const u64 b = block_index(p, x, ci) * p.wpb;
+                bool ok = true;
+                for (u32 w = 0; w < p.wpb; ++w) ok &= (__ldg(words + b + w) & mask[w]) == mask[w];
+                found = ok;
+            }
+            if (out) out[i] = (u8)found;
+            my_hits += found ? 1u : 0u;
+        } else {
+            insert_generic(p, words, x, mask);
+        }
+    }
+    if (OP == OP_CONTAINS && hits != nullptr) {
+        for (int o = 16; o > 0; o >>= 1) my_hits += __shfl_xor_sync(kFull, my_hits, o);
+        if ((threadIdx.x & 31) == 0 && my_hits) atomicAdd(hits, (unsigned long long)my_hits);
+    }
+}
+
+// Exact stream order for c >= 2 (reference _kernels.py:133-174 is sequential).
+// Keys of a chunk are applied in rounds: a pending key commits in a round iff
+// it holds the smallest pending index on every one of its candidate blocks
+// (claims are atomicMin'd into owner[]).  Committed keys of one round touch
+// pairwise-disjoint blocks, and every earlier key sharing a block with them
+// has already committed, so the result equals the sequential one.  Claims
+// carry (~round) in the high word, so stale owner[] values of older rounds
+// always lose and the array never needs clearing.
+__global__ void __launch_bounds__(256) ordered_kernel(const __grid_constant__ KParams p,
+                                                      u64 *__restrict__ words,
+                                                      const u64 *__restrict__ keys, u64 n,
+                                                      u64 chunk, u64 *__restrict__ owner,
+                                                      u32 *__restrict__ lists,
+                                                      u32 *__restrict__ state) {
+    cg::grid_group grid = cg::this_grid();
+    const u64 gtid = blockIdx.x * (u64)blockDim.x + threadIdx.x;
+    const u64 gstride = (u64)gridDim.x * blockDim.x;
+    u32 round = __ldcg(state);
+    u32 *cur = lists, *nxt = lists + chunk;
+    u64 mask[kMaxWpb];
+    for (u64 c0 = 0; c0 < n; c0 += chunk) {
+        u32 npend = (u32)min(chunk, n - c0);
+        bool first = true;
+        while (npend) {
+            const u64 claim_hi = (u64)(0xffffffffu - round) << 32;
+            u32 *cnt = state + 1 + (round & 1u);
+            if (gtid == 0) *cnt = 0;
+            for (u64 t = gtid; t < npend; t += gstride) {
+                const u32 li = first ? (u32)t : __ldcg(cur + t);
+                const u64 x = keys[c0 + li];
+                for (u32 ci = 0; ci < p.c; ++ci)
+                    atomicMin((unsigned long long *)(owner + block_index(p, x, ci)),
+                              (unsigned long long)(claim_hi | li));
+            }
+            grid.sync();
+            for (u64 t = gtid; t < npend; t += gstride) {
+                const u32 li = first ? (u32)t : __ldcg(cur + t);
+                const u64 x = keys[c0 + li];
+                bool win = true;
+                for (u32 ci = 0; ci < p.c; ++ci)
+                    win &= __ldcg(owner + block_index(p, x, ci)) == (claim_hi | li);
+                if (win) {
+                    build_mask_generic(p, x, mask);
+                    insert_generic(p, words, x, mask);
+                } else {
+                    nxt[atomicAdd(cnt, 1u)] = li;
+                }
+            }
+            grid.sync();
+            npend = __ldcg(cnt);
+            u32 *tmp = cur;
+            cur = nxt;
+            nxt = tmp;
+            first = false;
+            ++round;
+        }
+    }
+    if (gtid == 0) state[0] = round;
+}
+
+template <int OP>
+__global__ void __launch_bounds__(256) flat_kernel(const __grid_constant__ KParams p,
+                                                   u64 *__restrict__ words,
+                                                   const u64 *__restrict__ keys, u64 n,
+                                                   u8 *__restrict__ out,
+                                                   unsigned long long *__restrict__ hits) {
+    u32 my_hits = 0;
+    const u64 stride = (u64)gridDim.x * blockDim.x;
+    for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < n; i += stride) {
+        const u64 x = ld_stream(keys + i);
+        bool ok = true;
+        for (u32 b = 0; b < p.k; ++b) {
+            const u64 f = hval(__ldg(&p.bits[b].a), x, p.flat_b, p.flat_magic, p.flat_mode,
+                               p.flat_shift);
+            const u64 bit = 1ull << (f & 63);
+            if (OP == OP_INSERT) {
+                atomicOr((unsigned long long *)(words + (f >> 6)), (unsigned long long)bit);
+            } else if ((__ldg(words + (f >> 6)) & bit) == 0) {
+                ok = false;
+                break;
+            }
+        }
+        if (OP == OP_CONTAINS) {
+            if (out) out[i] = (u8)ok;
+            my_hits += ok ? 1u : 0u;
+        }
+    }
+    if (OP == OP_CONTAINS && hits != nullptr) {
+        for (int o = 16; o > 0; o >>= 1) my_hits += __shfl_xor_sync(kFull, my_hits, o);
+        if ((threadIdx.x & 31) == 0 && my_hits) atomicAdd(hits, (unsigned long long)my_hits);
+    }
+}
+
+// 512-bit blocks: four lanes per block, one coalesced LDG.128 each.
+__global__ void __launch_bounds__(256) hist512_kernel(const u64 *__restrict__ words,
+                                                      u64 num_blocks,
+                                                      unsigned long long *__restrict__ counts) {
+    __shared__ u32 sh[513];
+    for (int j = threadIdx.x; j < 513; j += blockDim.x) sh[j] = 0;
+    __syncthreads();
+    const uint4 *w4 = reinterpret_cast<const uint4 *>(words);
+    const u64 lanes = (u64)gridDim.x * blockDim.x;
+    const u64 total = num_blocks * 4;
+    // iterate in whole warps so the 4-lane shuffles see full groups
+    for (u64 i0 = (blockIdx.x * (u64)blockDim.x + threadIdx.x) & ~31ull; i0 < total;
+         i0 += lanes) {
+        const u64 i = i0 + (threadIdx.x & 31);
+        u32 c = i < total ? popc4(ld_block_nc(w4 + i)) : 0u;
+        c += __shfl_xor_sync(kFull, c, 1);
+        c += __shfl_xor_sync(kFull, c, 2);
+        if ((i & 3) == 0 && i < total) atomicAdd(&sh[c], 1u);
+    }
+    __syncthreads();
+    for (int j = threadIdx.x; j < 513; j += blockDim.x)
+        if (sh[j]) atomicAdd(counts + j, (unsigned long long)sh[j]);
+}
+
+__global__ void __launch_bounds__(256) hist_generic_kernel(const u64 *__restrict__ words,
+                                                           u64 num_blocks, u32 wpb,
+                                                           unsigned long long *__restrict__ counts) {
+    const u64 stride = (u64)gridDim.x * blockDim.x;
+    for (u64 b = blockIdx.x * (u64)blockDim.x + threadIdx.x; b < num_blocks; b += stride) {
+        u32 c = 0;
+        for (u32 w = 0; w < wpb; ++w) c += (u32)__popcll(__ldg(words + b * wpb + w));
+        atomicAdd(counts + c, 1ull);
+    }
+}
+
+__global__ void __launch_bounds__(256) eval_hash_kernel(DevHash h, const u64 *__restrict__ keys,
+                                                        u64 n, u64 *__restrict__ out) {
+    const u64 stride = (u64)gridDim.x * blockDim.x;
+    for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < n; i += stride)
+        out[i] = hval(h, keys[i]);
+}
+
+// ---------------------------------------------------------------------------------
+template <int OP, int C>
+static cudaError_t launch512(const KParams &p, u64 *words, const u64 *keys, u64 n, u8 *out,
+                             unsigned long long *hits, cudaStream_t s) {
+    const void *fn = (const void *)blocks512_kernel<OP, C>;
+    const unsigned grid = grid_for(fn, kTPB, 0, (n + kTPB - 1) / kTPB);
+    blocks512_kernel<OP, C><<<grid, kTPB, 0, s>>>(p, words, keys, n, out, hits);
+    count_launch();
+    return cudaGetLastError();
+}
+
+template <int OP>
+static cudaError_t launch512_c(const KParams &p, u64 *words, const u64 *keys, u64 n, u8 *out,
+                               unsigned long long *hits, cudaStream_t s) {
+    switch (p.c) {
+        case 1: return launch512<OP, 1>(p, words, keys, n, out, hits, s);
+        case 2: return launch512<OP, 2>(p, words, keys, n, out, hits, s);
+        case 3: return launch512<OP, 3>(p, words, keys, n, out, hits, s);
+        case 4: return launch512<OP, 4>(p, words, keys, n, out, hits, s);
+        case 5: return launch512<OP, 5>(p, words, keys, n, out, hits, s);
+        case 6: return launch512<OP, 6>(p, words, keys, n, out, hits, s);
+        case 7: return launch512<OP, 7>(p, words, keys, n, out, hits, s);
+        case 8: return launch512<OP, 8>(p, words, keys, n, out, hits, s);
+    }
+    return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_blocks(int op, const KParams &p, u64 *words, const u64 *keys, u64 n, u8 *out,
+                          unsigned long long *hits, cudaStream_t s) {
+    if (n == 0) return cudaSuccess;
+    if (p.wpb == 8) {
+        return op == OP_CONTAINS ? launch512_c<OP_CONTAINS>(p, words, keys, n, out, hits, s)
+                                 : launch512_c<OP_INSERT>(p, words, keys, n, out, hits, s);
+    }
+    const void *fn = op == OP_CONTAINS ? (const void *)generic_kernel<OP_CONTAINS>
+                                       : (const void *)generic_kernel<OP_INSERT>;
+    const unsigned grid = grid_for(fn, 256, 0, (n + 255) / 256);
+    if (op == OP_CONTAINS)
+        generic_kernel<OP_CONTAINS><<<grid, 256, 0, s>>>(p, words, keys, n, out, hits);
+    else
+        generic_kernel<OP_INSERT><<<grid, 256, 0, s>>>(p, words, keys, n, out, hits);
+    count_launch();
+    return cudaGetLastError();
+}
+
+cudaError_t launch_ordered(const KParams &p, u64 *words, const u64 *keys, u64 n, u64 chunk,
+                           u64 *owner, u32 *lists, u32 *state, cudaStream_t s) {
+    if (n == 0) return cudaSuccess;
+    const void *fn = (const void *)ordered_kernel;
+    const unsigned grid = grid_for(fn, 256, 0, (chunk + 255) / 256);
+    KParams pp = p;
+    void *args[] = {(void *)&pp, (void *)&words, (void *)&keys, (void *)&n,
+                    (void *)&chunk, (void *)&owner, (void *)&lists, (void *)&state};
+    cudaError_t e = cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(256), args, 0, s);
+    count_launch();
+    return e;
+}
+
+cudaError_t launch_flat(int op, const KParams &p, u64 *words, const u64 *keys, u64 n, u8 *out,
+                        unsigned long long *hits, cudaStream_t s) {
+    if (n == 0) return cudaSuccess;
+    const void *fn = op == OP_CONTAINS ? (const void *)flat_kernel<OP_CONTAINS>
+                                       : (const void *)flat_kernel<OP_INSERT>;
+    const unsigned grid = grid_for(fn, 256, 0, (n + 255) / 256);
+    if (op == OP_CONTAINS)
+        flat_kernel<OP_CONTAINS><<<grid, 256, 0, s>>>(p, words, keys, n, out, hits);
+    else
+        flat_kernel<OP_INSERT><<<grid, 256, 0, s>>>(p, words, keys, n, out, hits);
+    count_launch();
+    return cudaGetLastError();
+}
+
+cudaError_t launch_histogram(const u64 *words, u64 num_blocks, int block_bits,
+                             unsigned long long *counts, cudaStream_t s) {
+    if (num_blocks == 0) return cudaSuccess;
+    if (block_bits == 512) {
+        const unsigned grid =
+            grid_for((const void *)hist512_kernel, 256, 0, (num_blocks * 4 + 255) / 256);
+        hist512_kernel<<<grid, 256, 0, s>>>(words, num_blocks, counts);
+    } else {
+        const u32 wpb = block_bits >= 64 ? (u32)(block_bits / 64) : 1u;
+        const unsigned grid =
+            grid_for((const void *)hist_generic_kernel, 256, 0, (num_blocks + 255) / 256);
+        hist_generic_kernel<<<grid, 256, 0, s>>>(words, num_blocks, wpb, counts);
+    }
+    count_launch();
+    return cudaGetLastError();
+}
+
+cudaError_t launch_eval_hash(DevHash h, const u64 *keys, u64 n, u64 *out, cudaStream_t s) {
+    if (n == 0) return cudaSuccess;
+    const unsigned grid = grid_for((const void *)eval_hash_kernel, 256, 0, (n + 255) / 256);
+    eval_hash_kernel<<<grid, 256, 0, s>>>(h, keys, n, out);
+    count_launch();
+    return cudaGetLastError();
+}
+
+}  // namespace bc

@@ -1,0 +1,53 @@
+// Host-side launchers shared between the kernel translation units and the C ABI.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include "common.cuh"
+
+namespace bc {
+
+enum Op : int { OP_CONTAINS = 0, OP_INSERT = 1 };
+
+// Kernel launch accounting (bc_launch_count()).
+void count_launch(unsigned n = 1);
+
+// Persistent-grid size: min(work_ctas, SMs x resident CTAs of `kernel`).
+unsigned grid_for(const void *kernel, int threads, size_t dyn_smem, unsigned long long work_ctas);
+
+// ---- blocked family (filter_kernels.cu) ---------------------------------------
+// One launch over n keys.  OP_INSERT with c == 1 is an order-free OR; with
+// c >= 2 it is the relaxed (atomic) insert -- the caller bounds n per launch.
+cudaError_t launch_blocks(int op, const KParams &p, u64 *words, const u64 *keys, u64 n,
+                          u8 *out, unsigned long long *hits, cudaStream_t s);
+
+// Exact stream-order insert for c >= 2 (claim rounds, one cooperative launch).
+cudaError_t launch_ordered(const KParams &p, u64 *words, const u64 *keys, u64 n, u64 chunk,
+                           u64 *owner, u32 *lists, u32 *state, cudaStream_t s);
+
+// ---- standard (flat) kind --------------------------------------------------------
+cudaError_t launch_flat(int op, const KParams &p, u64 *words, const u64 *keys, u64 n, u8 *out,
+                        unsigned long long *hits, cudaStream_t s);
+
+// ---- utilities -------------------------------------------------------------------
+cudaError_t launch_histogram(const u64 *words, u64 num_blocks, int block_bits,
+                             unsigned long long *counts, cudaStream_t s);
+cudaError_t launch_eval_hash(DevHash h, const u64 *keys, u64 n, u64 *out, cudaStream_t s);
+
+// ---- q-grams (qgram_kernels.cu) ----------------------------------------------------
+// Valid windows per tile of kQgramTile windows, then an exclusive scan.
+constexpr int kQgramThreads = 256;
+constexpr int kQgramPerThread = 8;
+constexpr int kQgramTile = kQgramThreads * kQgramPerThread;
+cudaError_t launch_qgram_offsets(const u8 *seq, u64 len, int q, u64 *tile_off, u64 ntiles,
+                                 unsigned long long *total, cudaStream_t s);
+cudaError_t launch_qgram_encode(const u8 *seq, u64 len, int q, int canonical,
+                                const u64 *tile_off, u64 *keys, cudaStream_t s);
+// Fused: encode + (insert | contains).  tile_off may be NULL when no ordered
+// output is needed (inserts, count-only lookups).
+cudaError_t launch_qgram_blocks(int op, const KParams &p, u64 *words, const u8 *seq, u64 len,
+                                int q, int canonical, const u64 *tile_off, u8 *out,
+                                unsigned long long *hits, unsigned long long *count,
+                                cudaStream_t s);
+
+}  // namespace bc
