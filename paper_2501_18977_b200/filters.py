@@ -384,9 +384,11 @@ class Filter:
         self.storage.device_modified()
         self.inserted += n
 
-    def contains_many(self, keys):
+    def contains_many(self, keys, out=None):
         """Membership per key: numpy bool for host keys, CUDA bool tensor for
-        device keys."""
+        device keys.  ``out`` (optional) receives the answers: a uint8/bool
+        numpy array (pinned memory is written directly by the copy engine) or
+        a CUDA tensor for device keys."""
         from ._device import as_device_u64, host_u64, is_device_tensor, ptr, stream_ptr
 
         dev = self.device
@@ -394,12 +396,21 @@ class Filter:
             words = self.storage.d_words
             if is_device_tensor(keys):
                 d_keys = as_device_u64(keys, dev)
-                out = torch.empty(d_keys.numel(), dtype=torch.uint8, device=dev)
-                check(lib().bc_contains(self.handle, ptr(words), ptr(d_keys), d_keys.numel(),
+                n = d_keys.numel()
+                if out is None:
+                    out = torch.empty(n, dtype=torch.uint8, device=dev)
+                elif not (is_device_tensor(out) and out.numel() == n and out.is_contiguous()
+                          and out.element_size() == 1):
+                    raise ValueError("out must be a contiguous 1-byte CUDA tensor of n elements")
+                check(lib().bc_contains(self.handle, ptr(words), ptr(d_keys), n,
                                         ptr(out), None, stream_ptr(dev)))
                 return out.view(torch.bool)
             h = host_u64(keys)
-            out = np.empty(h.shape[0], dtype=np.uint8)
+            if out is None:
+                out = np.empty(h.shape[0], dtype=np.uint8)
+            elif not (isinstance(out, np.ndarray) and out.shape == (h.shape[0],)
+                      and out.dtype.itemsize == 1 and out.flags.c_contiguous):
+                raise ValueError("out must be a contiguous 1-byte numpy array of n elements")
             check(lib().bc_contains_host(self.handle, ptr(words), h.ctypes.data, h.shape[0],
                                          out.ctypes.data, None, stream_ptr(dev)))
             return out.view(np.bool_)
