@@ -1,16 +1,20 @@
 // Per-key work of the blocked family, shared by the key-array kernels
 // (filter_kernels.cu) and the fused q-gram kernels (qgram_kernels.cu).
 //
-// 512-bit blocks (the reference's default, one 64-byte line) use a two-phase
-// tile of kTPB keys per CTA iteration:
+// 512-bit blocks (the reference's default, one 64-byte line) are processed
+// by each warp in tiles of 32 keys, warp-synchronously (no CTA barrier):
 //
-//   phase 1, one thread per key: hash the key (shard + c block hashes + k
-//     bit hashes) and build its 512-bit bit mask in shared memory
-//     (layout mask[word32][key], so lanes touch distinct banks);
-//   phase 2, four lanes per key: lane s owns bytes [16s, 16s+16) of every
-//     block, so one warp-wide LDG.128 moves eight whole 64-byte blocks (one
-//     L1 wavefront per block instead of four) and the test / popcount /
-//     atomic OR of a block is spread over the four lanes.
+//   phase 1, one lane per key: hash the key (shard + c block hashes + k
+//     bit hashes) and build its 512-bit mask in the warp's shared-memory
+//     slice, layout mask[word][key] -- every access of a lane hits bank
+//     `lane`, so the data-dependent word index never causes a conflict;
+//   phase 2, four lanes per key: group g (lanes 4g..4g+3) handles keys
+//     4g..4g+3 of the tile in four passes; lane s owns bytes [16s, 16s+16)
+//     of every block, so one warp-wide LDG.128 moves eight whole 64-byte
+//     blocks (one L1 wavefront per block instead of four).  The masks of
+//     all four passes are read up front in a rotated order (lane s reads
+//     key 4g + ((p + s) & 3) in read p), which makes those 16 reads per lane
+//     bank-conflict-free; the right slot is then selected per pass.
 //
 // Semantics follow _kernels.py:112-211 exactly: membership = any choice
 // whose block holds every address; insert with c == 1 ORs the mask; with
@@ -25,16 +29,14 @@
 
 namespace bc {
 
-constexpr int kTPB = 256;            // keys per tile == threads per CTA
-constexpr int kGroups = kTPB / 4;    // keys per phase-2 pass
-constexpr int kPasses = kTPB / kGroups;
+constexpr int kTPB = 256;      // threads per CTA
+constexpr int kWarps = kTPB / 32;
 constexpr u32 kFull = 0xffffffffu;
 
 template <int C>
-struct TileSmem {
-    u32 mask[16][kTPB];   // 512-bit masks, word-major
-    u32 blk[C][kTPB];     // candidate block indices
-    u8 out[kTPB];         // lookup answers of the tile
+struct WarpSmem {
+    u32 mask[16][32];  // 512-bit masks of the warp's 32 keys, word-major
+    u32 blk[C][32];    // candidate block indices
 };
 
 __device__ __forceinline__ DevHash load_hash(const DevHash *h) {
@@ -47,25 +49,25 @@ __device__ __forceinline__ DevHash load_hash(const DevHash *h) {
     return r;
 }
 
-// ---- phase 1: one thread per key ------------------------------------------------
+// ---- phase 1: one lane per key ----------------------------------------------------
 template <int C>
-__device__ __forceinline__ void phase1(const KParams &p, u64 x, bool valid, TileSmem<C> &sm,
-                                       int tid) {
-    u32 *col = &sm.mask[0][tid];
+__device__ __forceinline__ void phase1(const KParams &p, u64 x, bool valid, WarpSmem<C> &ws,
+                                       int lane) {
+    u32 *col = &ws.mask[0][lane];
 #pragma unroll
-    for (int w = 0; w < 16; ++w) col[w * kTPB] = 0u;
+    for (int w = 0; w < 16; ++w) col[w * 32] = 0u;
     if (valid) {
         if (p.fast_random) {
             const u32 xlo = (u32)x, xhi = (u32)(x >> 32);
 #pragma unroll 4
             for (u32 i = 0; i < p.k; ++i) {
                 u32 h = bit512(p.bit_a_lo[i], p.bit_a_hi[i], xlo, xhi);
-                col[(h >> 5) * kTPB] |= 1u << (h & 31);
+                col[(h >> 5) * 32] |= 1u << (h & 31);
             }
         } else if (p.strategy == 0) {
             for (u32 i = 0; i < p.k; ++i) {
                 u32 h = (u32)hval(load_hash(p.bits + i), x);
-                col[(h >> 5) * kTPB] |= 1u << (h & 31);
+                col[(h >> 5) * 32] |= 1u << (h & 31);
             }
         } else {
             // distinct: the r-th address not chosen so far (hashing.py:181-200),
@@ -74,84 +76,108 @@ __device__ __forceinline__ void phase1(const KParams &p, u64 x, bool valid, Tile
                 u32 r = (u32)hval(load_hash(p.bits + i), x);
                 u32 w = 0;
                 for (;; ++w) {
-                    u32 z = 32u - __popc(col[w * kTPB]);
+                    u32 z = 32u - __popc(col[w * 32]);
                     if (r < z) break;
                     r -= z;
                 }
-                u32 pos = select_bit32(~col[w * kTPB], r);
-                col[w * kTPB] |= 1u << pos;
+                col[w * 32] |= 1u << select_bit32(~col[w * 32], r);
             }
         }
     }
 #pragma unroll
-    for (int ci = 0; ci < C; ++ci) sm.blk[ci][tid] = valid ? (u32)block_index(p, x, ci) : 0u;
+    for (int ci = 0; ci < C; ++ci) ws.blk[ci][lane] = valid ? (u32)block_index(p, x, ci) : 0u;
 }
 
 __device__ __forceinline__ u32 popc4(uint4 v) {
     return __popc(v.x) + __popc(v.y) + __popc(v.z) + __popc(v.w);
 }
 
+// every mask bit set in w: (m & ~w) == 0, folded with LOP3s
 __device__ __forceinline__ bool covers(uint4 w, uint4 m) {
-    return ((w.x & m.x) == m.x) & ((w.y & m.y) == m.y) & ((w.z & m.z) == m.z) &
-           ((w.w & m.w) == m.w);
+    return ((m.x & ~w.x) | (m.y & ~w.y) | (m.z & ~w.z) | (m.w & ~w.w)) == 0u;
 }
 
-// ---- phase 2: four lanes per key ---------------------------------------------------
-// Returns the number of hits among valid keys handled by this lane (lookups).
+// r = p ? a : b as a SEL (keeps ptxas from turning the lane-divergent
+// selection into branches)
+__device__ __forceinline__ u32 selp(u32 a, u32 b, u32 p) {
+    u32 r;
+    asm("{.reg .pred q; setp.ne.u32 q, %3, 0; selp.b32 %0, %1, %2, q;}"
+        : "=r"(r)
+        : "r"(a), "r"(b), "r"(p));
+    return r;
+}
+
+__device__ __forceinline__ uint4 selp4(const uint4 &a, const uint4 &b, u32 p) {
+    return make_uint4(selp(a.x, b.x, p), selp(a.y, b.y, p), selp(a.z, b.z, p),
+                      selp(a.w, b.w, p));
+}
+
+// M[i] for a lane-dependent i in [0, 4): two levels of SELs, no branches.
+__device__ __forceinline__ uint4 sel4(const uint4 (&M)[4], int i) {
+    const uint4 lo = selp4(M[1], M[0], i & 1);
+    const uint4 hi = selp4(M[3], M[2], i & 1);
+    return selp4(hi, lo, i & 2);
+}
+
+// ---- phase 2: four lanes per key -------------------------------------------------
+// Lookups: returns the answers of the group's four keys packed one per byte
+// (key 4g + p in byte p), identical in the four lanes of the group.
 template <int OP, int C>
-__device__ __forceinline__ u32 phase2(const KParams &p, u64 *words, TileSmem<C> &sm, u32 cnt,
-                                      int tid) {
+__device__ __forceinline__ u32 phase2(const KParams &p, u64 *words, WarpSmem<C> &ws,
+                                      int lane) {
     constexpr bool kNoLoad = (OP == OP_INSERT && C == 1);
     constexpr int UNR = kNoLoad ? 4 : (C <= 2 ? 4 : (C <= 4 ? 2 : 1));
     constexpr int CL = kNoLoad ? 1 : C;
-    const int g = tid >> 2, s = tid & 3, lane = tid & 31;
+    const int g = lane >> 2, s = lane & 3;
     const uint4 *w4 = reinterpret_cast<const uint4 *>(words);
-    u32 hits = 0;
+    uint4 M[4];
 #pragma unroll
-    for (int p0 = 0; p0 < kPasses; p0 += UNR) {
-        uint4 m[UNR];
+    for (int r = 0; r < 4; ++r) {
+        const int kr = 4 * g + ((r + s) & 3);
+        M[r] = make_uint4(ws.mask[4 * s][kr], ws.mask[4 * s + 1][kr], ws.mask[4 * s + 2][kr],
+                          ws.mask[4 * s + 3][kr]);
+    }
+    u32 found_bytes = 0;
+#pragma unroll
+    for (int p0 = 0; p0 < 4; p0 += UNR) {
         uint4 w[UNR][CL];
+        if (!kNoLoad) {
 #pragma unroll
-        for (int u = 0; u < UNR; ++u) {
-            const int kk = (p0 + u) * kGroups + g;
-            m[u] = make_uint4(sm.mask[4 * s][kk], sm.mask[4 * s + 1][kk], sm.mask[4 * s + 2][kk],
-                              sm.mask[4 * s + 3][kk]);
-            if (!kNoLoad) {
+            for (int u = 0; u < UNR; ++u) {
+                const int kk = 4 * g + p0 + u;
 #pragma unroll
                 for (int ci = 0; ci < C; ++ci) {
-                    const u64 b = sm.blk[ci][kk];
-                    w[u][ci] = OP == OP_CONTAINS ? ld_block_nc(w4 + b * 4 + s)
-                                                 : ld_block_cg(w4 + b * 4 + s);
+                    const u64 b = ws.blk[ci][kk];
+                    w[u][ci] = ld_block_cg(w4 + b * 4 + s);
                 }
             }
         }
 #pragma unroll
         for (int u = 0; u < UNR; ++u) {
-            const int kk = (p0 + u) * kGroups + g;
-            const u64 lo = (u64)m[u].x | ((u64)m[u].y << 32);
-            const u64 hi = (u64)m[u].z | ((u64)m[u].w << 32);
+            const int pass = p0 + u;
+            const int kk = 4 * g + pass;
+            const uint4 m = sel4(M, (pass - s) & 3);
+            const u64 lo = (u64)m.x | ((u64)m.y << 32);
+            const u64 hi = (u64)m.z | ((u64)m.w << 32);
             if (OP == OP_CONTAINS) {
                 bool found = false;
 #pragma unroll
                 for (int ci = 0; ci < CL; ++ci) {
-                    u32 bal = __ballot_sync(kFull, covers(w[u][ci], m[u]));
+                    const u32 bal = __ballot_sync(kFull, covers(w[u][ci], m));
                     found |= ((bal >> (lane & 28)) & 0xFu) == 0xFu;
                 }
-                if (s == 0) {
-                    sm.out[kk] = (u8)found;
-                    hits += (found && (u32)kk < cnt) ? 1u : 0u;
-                }
+                found_bytes |= (found ? 1u : 0u) << (8 * pass);
             } else if (C == 1) {
-                u64 *dst = words + (u64)sm.blk[0][kk] * 8 + 2 * s;
+                u64 *dst = words + (u64)ws.blk[0][kk] * 8 + 2 * s;
                 red_or(dst, lo);
                 red_or(dst + 1, hi);
             } else {
                 u32 v[CL];
 #pragma unroll
                 for (int ci = 0; ci < CL; ++ci) {
-                    uint4 ww = w[u][ci];
-                    uint4 uni = make_uint4(ww.x | m[u].x, ww.y | m[u].y, ww.z | m[u].z,
-                                           ww.w | m[u].w);
+                    const uint4 ww = w[u][ci];
+                    const uint4 uni =
+                        make_uint4(ww.x | m.x, ww.y | m.y, ww.z | m.z, ww.w | m.w);
                     u32 t = popc4(uni) | (popc4(ww) << 16);
                     t += __shfl_xor_sync(kFull, t, 1);
                     t += __shfl_xor_sync(kFull, t, 2);
@@ -177,14 +203,40 @@ __device__ __forceinline__ u32 phase2(const KParams &p, u64 *words, TileSmem<C> 
                     }
                 }
                 if (!noop) {
-                    u64 *dst = words + (u64)sm.blk[best][kk] * 8 + 2 * s;
+                    u64 *dst = words + (u64)ws.blk[best][kk] * 8 + 2 * s;
                     red_or(dst, lo);
                     red_or(dst + 1, hi);
                 }
             }
         }
     }
-    return hits;
+    return found_bytes;
+}
+
+// Write the group's four answers (keys 4g..4g+3 of a 32-key tile at `base`)
+// and count hits among the first `cnt` keys of the tile.
+__device__ __forceinline__ u32 emit_answers(u8 *out, u64 base, u32 cnt, u32 found_bytes,
+                                            int lane) {
+    const int g = lane >> 2, s = lane & 3;
+    const u32 first = 4u * g;
+    u32 valid_bytes = 0;
+    if (first + 4 <= cnt) {
+        valid_bytes = 0x01010101u;
+    } else {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) valid_bytes |= (first + i < cnt ? 1u : 0u) << (8 * i);
+    }
+    const u32 f = found_bytes & valid_bytes;
+    if (out != nullptr && s == 0) {
+        u8 *dst = out + base + first;
+        if (valid_bytes == 0x01010101u && ((uintptr_t)dst & 3u) == 0) {
+            *reinterpret_cast<u32 *>(dst) = f;
+        } else {
+            for (int i = 0; i < 4; ++i)
+                if (first + i < cnt) out[base + first + i] = (u8)((f >> (8 * i)) & 1u);
+        }
+    }
+    return s == 0 ? (u32)__popc(f) : 0u;
 }
 
 // ---- thread-per-key building blocks (any block width, ordered inserts) -------------

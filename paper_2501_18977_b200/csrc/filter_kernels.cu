@@ -64,24 +64,27 @@ __global__ void __launch_bounds__(kTPB) blocks512_kernel(const __grid_constant__
                                                          const u64 *__restrict__ keys, u64 n,
                                                          u8 *__restrict__ out,
                                                          unsigned long long *__restrict__ hits) {
-    __shared__ TileSmem<C> sm;
-    const int tid = threadIdx.x;
-    const u64 ntiles = (n + kTPB - 1) / kTPB;
+    __shared__ WarpSmem<C> smem[kWarps];
+    WarpSmem<C> &ws = smem[threadIdx.x >> 5];
+    const int lane = threadIdx.x & 31;
+    const u64 ntiles = (n + 31) / 32;
+    const u64 nwarps = (u64)gridDim.x * kWarps;
     u32 my_hits = 0;
-    for (u64 tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        const u64 base = tile * kTPB;
-        const u32 cnt = (u32)min((u64)kTPB, n - base);
-        const bool valid = (u32)tid < cnt;
-        const u64 x = valid ? ld_stream(keys + base + tid) : 0ull;
-        phase1<C>(p, x, valid, sm, tid);
-        __syncthreads();
-        my_hits += phase2<OP, C>(p, words, sm, cnt, tid);
-        __syncthreads();
-        if (OP == OP_CONTAINS && out != nullptr && valid) out[base + tid] = sm.out[tid];
+    for (u64 tile = blockIdx.x * (u64)kWarps + (threadIdx.x >> 5); tile < ntiles;
+         tile += nwarps) {
+        const u64 base = tile * 32;
+        const u32 cnt = (u32)min((u64)32, n - base);
+        const bool valid = (u32)lane < cnt;
+        const u64 x = valid ? ld_stream(keys + base + lane) : 0ull;
+        phase1<C>(p, x, valid, ws, lane);
+        __syncwarp();
+        const u32 found = phase2<OP, C>(p, words, ws, lane);
+        if (OP == OP_CONTAINS) my_hits += emit_answers(out, base, cnt, found, lane);
+        __syncwarp();
     }
     if (OP == OP_CONTAINS && hits != nullptr) {
         for (int o = 16; o > 0; o >>= 1) my_hits += __shfl_xor_sync(kFull, my_hits, o);
-        if ((tid & 31) == 0 && my_hits) atomicAdd(hits, (unsigned long long)my_hits);
+        if (lane == 0 && my_hits) atomicAdd(hits, (unsigned long long)my_hits);
     }
 }
 

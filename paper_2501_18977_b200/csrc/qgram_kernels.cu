@@ -175,29 +175,31 @@ __global__ void __launch_bounds__(kQgramThreads) qgram_blocks_kernel(
     u64 len, int q, int canonical, u64 nwin, u64 ntiles, const u64 *__restrict__ tile_off,
     u8 *__restrict__ out, unsigned long long *__restrict__ hits,
     unsigned long long *__restrict__ count) {
-    static_assert(kQgramThreads == kTPB, "tile pipeline assumes one thread per key");
+    static_assert(kQgramThreads == kTPB, "tile pipeline assumes the CTA shape of blocks.cuh");
     __shared__ QgramSmem qs;
-    __shared__ TileSmem<C> sm;
-    const int tid = threadIdx.x;
+    __shared__ WarpSmem<C> smem[kWarps];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    WarpSmem<C> &ws = smem[warp];
     u32 my_hits = 0;
     for (u64 tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         const u32 v = tile_encode(seq, len, q, canonical, tile * kQgramTile, nwin, qs);
         const u64 obase = (OP == OP_CONTAINS && tile_off) ? tile_off[tile] : 0ull;
         if (count != nullptr && tid == 0 && v) atomicAdd(count, (unsigned long long)v);
-        for (u32 sub = 0; sub < v; sub += kTPB) {
-            const u32 cnt = min((u32)kTPB, v - sub);
-            const bool valid = (u32)tid < cnt;
-            phase1<C>(p, valid ? qs.keys[sub + tid] : 0ull, valid, sm, tid);
-            __syncthreads();
-            my_hits += phase2<OP, C>(p, words, sm, cnt, tid);
-            __syncthreads();
-            if (OP == OP_CONTAINS && out != nullptr && valid) out[obase + sub + tid] = sm.out[tid];
+        // each warp takes 32 consecutive compacted keys at a time
+        for (u32 sub = 32u * warp; sub < v; sub += 32u * kWarps) {
+            const u32 cnt = min(32u, v - sub);
+            const bool valid = (u32)lane < cnt;
+            phase1<C>(p, valid ? qs.keys[sub + lane] : 0ull, valid, ws, lane);
+            __syncwarp();
+            const u32 found = phase2<OP, C>(p, words, ws, lane);
+            if (OP == OP_CONTAINS) my_hits += emit_answers(out, obase + sub, cnt, found, lane);
+            __syncwarp();
         }
         __syncthreads();
     }
     if (OP == OP_CONTAINS && hits != nullptr) {
         for (int o = 16; o > 0; o >>= 1) my_hits += __shfl_xor_sync(kFull, my_hits, o);
-        if ((tid & 31) == 0 && my_hits) atomicAdd(hits, (unsigned long long)my_hits);
+        if (lane == 0 && my_hits) atomicAdd(hits, (unsigned long long)my_hits);
     }
 }
 

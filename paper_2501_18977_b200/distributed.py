@@ -1,0 +1,188 @@
+"""Multi-GPU layer: one process per GPU, torch.distributed (NCCL) plumbing.
+
+Two data-parallel patterns, both from the reference's own parallel design
+(sharding.py:1-136, analysis.py:96-107):
+
+* **Lookups shard by key over replicas.**  Every rank holds a full copy of
+  the bit array (NCCL broadcast from the rank that built it); a key batch is
+  split into contiguous per-rank slices, each rank answers its slice with
+  the lookup kernel, and answers are all-gathered (or hit counts
+  all-reduced).  The lookup itself has no communication, so it scales with
+  the number of GPUs; the one-time broadcast is reported separately.
+
+* **Inserts go to hash-partitioned subfilters only where the reference's
+  layout has them** (``shards = T > 1``).  Shard s owns words
+  [s*wps, (s+1)*wps); rank r owns the contiguous shard range
+  [r*T/W, (r+1)*T/W).  Keys are routed with the shard hash h0 on the
+  device; each rank inserts, in stream order, the keys of its shards only
+  (so ordered builds stay bit-identical to the reference's sequential
+  build, sharding.py:1-9), then an all-gather of the W contiguous word
+  ranges replicates the filter.  With T = 1 (every BASELINE config) rank 0
+  builds and broadcasts.
+
+Every collective acts on the filter's word tensor; no collective runs inside
+a lookup or insert kernel.  The functions only use the filter's public
+interface (``route_many``, ``insert_many``, ``contains_many``,
+``count_hits``, ``storage.d_words``), so the orchestration is tested on CPU
+with gloo and the oracle standing in for the kernels.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+
+def _rank_world(group):
+    return dist.get_rank(group), dist.get_world_size(group)
+
+
+def _words_i64(filt) -> torch.Tensor:
+    return filt.storage.d_words.view(torch.int64)
+
+
+def slice_bounds(n: int, world: int) -> list:
+    """Contiguous [lo, hi) per rank (np.array_split sizing, analysis.py:103)."""
+    base, extra = divmod(n, world)
+    bounds, lo = [], 0
+    for r in range(world):
+        hi = lo + base + (1 if r < extra else 0)
+        bounds.append((lo, hi))
+        lo = hi
+    return bounds
+
+
+def broadcast_filter(filt, src: int = 0, group=None) -> None:
+    """Replicate the bit array (and the inserted-key count) from ``src``."""
+    dist.broadcast(_words_i64(filt), src=src, group=group)
+    meta = torch.tensor([filt.inserted], dtype=torch.int64,
+                        device=filt.storage.d_words.device)
+    dist.broadcast(meta, src=src, group=group)
+    filt.inserted = int(meta.item())
+    filt.storage.device_modified()
+
+
+def _local_slice(keys, group):
+    rank, world = _rank_world(group)
+    lo, hi = slice_bounds(len(keys), world)[rank]
+    return keys[lo:hi], lo, hi
+
+
+def contains_many_sharded(filt, keys, group=None, gather: bool = True):
+    """Key-sharded lookup on replicated filters.  ``keys`` is the full batch
+    (identical on every rank); each rank answers its contiguous slice.
+    Returns the full answer array on every rank (``gather``), else this
+    rank's slice."""
+    rank, world = _rank_world(group)
+    part, lo, hi = _local_slice(keys, group)
+    ans = filt.contains_many(part)
+    if not gather or world == 1:
+        return ans
+    dev = filt.storage.d_words.device
+    bounds = slice_bounds(len(keys), world)
+    width = max(h - l for l, h in bounds)
+    local = torch.zeros(width, dtype=torch.uint8, device=dev)
+    a = torch.as_tensor(np.asarray(ans) if not isinstance(ans, torch.Tensor) else ans)
+    local[: hi - lo] = a.to(device=dev, dtype=torch.uint8)
+    outs = [torch.empty(width, dtype=torch.uint8, device=dev) for _ in range(world)]
+    dist.all_gather(outs, local, group=group)
+    full = torch.cat([o[: h - l] for o, (l, h) in zip(outs, bounds)]).bool()
+    return full if isinstance(keys, torch.Tensor) and keys.is_cuda else full.cpu().numpy()
+
+
+def count_hits_sharded(filt, keys, group=None) -> int:
+    """Hits over the whole batch: per-rank count + all-reduce(sum)."""
+    part, _, _ = _local_slice(keys, group)
+    hits = torch.tensor([filt.count_hits(part)], dtype=torch.int64,
+                        device=filt.storage.d_words.device)
+    dist.all_reduce(hits, group=group)
+    return int(hits.item())
+
+
+def _as_numpy_u64(keys) -> np.ndarray:
+    if isinstance(keys, torch.Tensor):
+        return keys.detach().cpu().view(torch.uint64).numpy() if keys.dtype == torch.int64 \
+            else keys.detach().cpu().numpy().astype(np.uint64)
+    return np.ascontiguousarray(keys, dtype=np.uint64)
+
+
+def owned_keys(filt, keys, rank: int, world: int):
+    """The keys of ``keys`` whose shard rank ``rank`` owns, in stream order."""
+    if filt.shards % world != 0:
+        raise ValueError(f"{filt.shards} shards do not split over {world} ranks")
+    per = filt.shards // world
+    shard = filt.route_many(keys)
+    if isinstance(shard, torch.Tensor):
+        sel = (shard >= rank * per) & (shard < (rank + 1) * per)
+        return keys[sel]
+    shard = np.asarray(shard)
+    sel = (shard >= rank * per) & (shard < (rank + 1) * per)
+    return np.asarray(keys)[sel]
+
+
+def gather_subfilters(filt, group=None) -> None:
+    """All-gather the W contiguous shard ranges so every rank holds the
+    whole bit array."""
+    rank, world = _rank_world(group)
+    words = _words_i64(filt)
+    span = words.numel() // world
+    mine = words[rank * span:(rank + 1) * span].clone()
+    parts = [words[r * span:(r + 1) * span] for r in range(world)]
+    if dist.get_backend(group) == "nccl":
+        dist.all_gather_into_tensor(words, mine, group=group)
+    else:
+        outs = [torch.empty_like(mine) for _ in range(world)]
+        dist.all_gather(outs, mine, group=group)
+        for p, o in zip(parts, outs):
+            p.copy_(o)
+    counts = torch.tensor([filt.inserted], dtype=torch.int64, device=words.device)
+    dist.all_reduce(counts, group=group)
+    filt.inserted = int(counts.item())
+    filt.storage.device_modified()
+
+
+def build_subfilters(filt, keys, group=None, mode: str | None = None):
+    """Insert a key stream (identical on every rank) into ``filt``.
+
+    ``shards > 1``: each rank inserts the keys of its shard range (device
+    routing, no data exchange), then the ranges are all-gathered.
+    ``shards == 1``: rank 0 inserts everything, then broadcasts."""
+    rank, world = _rank_world(group)
+    if filt.shards == 1 or world == 1:
+        if rank == 0:
+            filt.insert_many(keys, mode=mode) if mode else filt.insert_many(keys)
+        if world > 1:
+            broadcast_filter(filt, src=0, group=group)
+        return filt
+    mine = owned_keys(filt, keys, rank, world)
+    before = filt.inserted
+    filt.insert_many(mine, mode=mode) if mode else filt.insert_many(mine)
+    filt.inserted = filt.inserted - before  # this rank's share; summed below
+    gather_subfilters(filt, group=group)
+    filt.inserted += before
+    return filt
+
+
+def exchange_by_shard(filt, local_keys, group=None):
+    """Route a rank-local slice of the stream to the shard owners
+    (all-to-all).  Rank r is assumed to hold the r-th contiguous part of the
+    stream; received pieces are concatenated in source-rank order, which
+    keeps every shard's stream order."""
+    rank, world = _rank_world(group)
+    per = filt.shards // world
+    keys = _as_numpy_u64(local_keys)
+    shard = np.asarray(filt.route_many(keys))
+    owner = shard // per
+    order = np.argsort(owner, kind="stable")
+    send = torch.from_numpy(keys[order].view(np.int64).copy())
+    send_counts = np.bincount(owner, minlength=world).astype(np.int64)
+    dev = filt.storage.d_words.device
+    sc = torch.from_numpy(send_counts).to(dev)
+    rc = torch.empty_like(sc)
+    dist.all_to_all_single(rc, sc, group=group)
+    recv_counts = rc.cpu().numpy()
+    recv = torch.empty(int(recv_counts.sum()), dtype=torch.int64, device=dev)
+    dist.all_to_all_single(recv, send.to(dev), output_split_sizes=recv_counts.tolist(),
+                           input_split_sizes=send_counts.tolist(), group=group)
+    return recv.view(torch.uint64) if dev.type == "cuda" else recv.numpy().view(np.uint64)

@@ -1,0 +1,123 @@
+"""Multi-process (gloo, world_size 2, CPU) tests of the multi-GPU orchestration
+in paper_2501_18977_b200.distributed.  The per-rank kernels are replaced by
+the CPU oracle through the same duck-typed filter interface, so what is
+tested is the partitioning, routing and collectives."""
+
+import os
+import socket
+from types import SimpleNamespace
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from oracle import oracle as orc
+
+
+def free_port() -> int:
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def np_hash(a: int, b: int, keys: np.ndarray) -> np.ndarray:
+    """hashing.py:90-100 restated in numpy (test-side)."""
+    ax = np.uint64(a) * keys
+    mode, s = orc.hash_branch(b)
+    if mode == 1:
+        return (ax >> np.uint64(s)) % np.uint64(b)
+    if mode == 2:
+        ax = ax ^ (ax >> np.uint64(s))
+    return ax % np.uint64(b)
+
+
+class OracleFilter:
+    """The filter interface distributed.py relies on, backed by the oracle."""
+
+    def __init__(self, **kw):
+        self.o = orc.make_filter(**kw)
+        self.shards = self.o.shards
+        self.inserted = 0
+        self.storage = SimpleNamespace(d_words=torch.from_numpy(self.o.words),
+                                       device_modified=lambda: None)
+
+    def route_many(self, keys):
+        return np_hash(self.o.shard_a, self.shards, np.asarray(keys, dtype=np.uint64))
+
+    def insert_many(self, keys, mode=None):
+        keys = np.asarray(keys, dtype=np.uint64)
+        self.o.insert_many(keys)
+        self.inserted += keys.shape[0]
+
+    def contains_many(self, keys):
+        return self.o.contains_many(np.asarray(keys, dtype=np.uint64))
+
+    def count_hits(self, keys):
+        return int(self.contains_many(keys).sum())
+
+
+CFG = dict(kind="blowchoc", k=7, choices=2, n_capacity=20_000, shards=4, seed=17)
+
+
+def _worker(rank, world, port, case):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2501_18977_b200 import distributed as D
+
+        keys = orc.even_keys(20_000, 5)
+        ref = orc.make_filter(**CFG)
+        ref.insert_many(keys)
+        if case == "subfilters":
+            f = OracleFilter(**CFG)
+            D.build_subfilters(f, keys)
+            assert np.array_equal(f.o.words, ref.words)
+            assert f.inserted == keys.shape[0]
+        elif case == "broadcast":
+            cfg1 = dict(CFG, shards=1)
+            ref1 = orc.make_filter(**cfg1)
+            ref1.insert_many(keys)
+            f = OracleFilter(**cfg1)
+            D.build_subfilters(f, keys)
+            assert np.array_equal(f.o.words, ref1.words)
+        elif case == "lookups":
+            f = OracleFilter(**CFG)
+            if rank == 0:
+                f.insert_many(keys)
+            D.broadcast_filter(f, src=0)
+            probes = np.concatenate([keys[:5000], orc.odd_keys(7001, 9)])
+            full = D.contains_many_sharded(f, probes)
+            assert np.array_equal(full, ref.contains_many(probes))
+            assert D.count_hits_sharded(f, probes) == int(ref.contains_many(probes).sum())
+        elif case == "exchange":
+            f = OracleFilter(**CFG)
+            lo, hi = D.slice_bounds(keys.shape[0], world)[rank]
+            mine = D.exchange_by_shard(f, keys[lo:hi])
+            per = f.shards // world
+            assert np.all(np.asarray(f.route_many(mine)) // per == rank)
+            f.insert_many(mine)
+            f.inserted = int(np.asarray(mine).shape[0])
+            D.gather_subfilters(f)
+            assert np.array_equal(f.o.words, ref.words)
+            assert f.inserted == keys.shape[0]
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("case", ["subfilters", "broadcast", "lookups", "exchange"])
+def test_two_rank_gloo(case):
+    mp.spawn(_worker, args=(2, free_port(), case), nprocs=2, join=True)
+
+
+def test_slice_bounds_cover():
+    from paper_2501_18977_b200.distributed import slice_bounds
+
+    for n in (0, 1, 7, 100, 2**20 + 3):
+        for w in (1, 2, 3, 8):
+            b = slice_bounds(n, w)
+            assert b[0][0] == 0 and b[-1][1] == n
+            assert all(b[i][1] == b[i + 1][0] for i in range(w - 1))
+            assert max(h - l for l, h in b) - min(h - l for l, h in b) <= 1

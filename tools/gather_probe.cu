@@ -1,0 +1,139 @@
+// Random 64-byte-block gather microbenchmark: the practical ceiling for the
+// lookup kernel (SURVEY §8(d) "random-64B-gather microbenchmark").
+//
+// Four lanes read one 64-byte block (one LDG.128 each), blocks chosen by a
+// splitmix hash of the lookup index, one 8-byte key streamed per lookup,
+// one byte written per lookup -- the lookup kernel's memory pattern without
+// its hashing.  Variants: cache-hint of the block load and the device L2
+// fetch granularity.
+//
+//   nvcc -O3 -gencode arch=compute_100a,code=sm_100a -o gather_probe tools/gather_probe.cu
+//   ./gather_probe <filter MiB> <lookups log2>
+#include <cuda_runtime.h>
+
+#include <cstdio>
+#include <cstdlib>
+#include <cstdint>
+
+typedef unsigned long long u64;
+
+__device__ __forceinline__ u64 mix(u64 z) {
+    z += 0x9E3779B97F4A7C15ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+
+template <int V>
+__device__ __forceinline__ uint4 ld(const uint4 *p) {
+    uint4 r;
+    if (V == 0)
+        asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+                     : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
+    else if (V == 1)
+        asm volatile("ld.global.cg.v4.u32 {%0,%1,%2,%3}, [%4];"
+                     : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
+    else if (V == 2)
+        asm volatile("ld.global.nc.L1::no_allocate.L2::64B.v4.u32 {%0,%1,%2,%3}, [%4];"
+                     : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
+    else if (V == 3)
+        asm volatile("ld.global.nc.L1::no_allocate.L2::128B.v4.u32 {%0,%1,%2,%3}, [%4];"
+                     : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
+    else
+        asm volatile("ld.global.nc.L1::no_allocate.L2::256B.v4.u32 {%0,%1,%2,%3}, [%4];"
+                     : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
+    return r;
+}
+
+// UNR lookups in flight per 4-lane group
+template <int V, int UNR>
+__global__ void __launch_bounds__(256) gather(const uint4 *__restrict__ blocks, u64 nblocks,
+                                              const u64 *__restrict__ keys, u64 n,
+                                              unsigned char *__restrict__ out) {
+    const int s = threadIdx.x & 3;
+    const u64 g0 = (blockIdx.x * (u64)blockDim.x + threadIdx.x) >> 2;
+    const u64 groups = ((u64)gridDim.x * blockDim.x) >> 2;
+    for (u64 base = g0; base < n; base += groups * UNR) {
+        uint4 w[UNR];
+#pragma unroll
+        for (int u = 0; u < UNR; ++u) {
+            const u64 i = base + u * groups;
+            const u64 x = i < n ? __ldcs(keys + i) : 0;
+            const u64 b = __umul64hi(mix(x), nblocks);
+            w[u] = ld<V>(blocks + b * 4 + s);
+        }
+#pragma unroll
+        for (int u = 0; u < UNR; ++u) {
+            const u64 i = base + u * groups;
+            const unsigned v = w[u].x ^ w[u].y ^ w[u].z ^ w[u].w;
+            const unsigned all = __reduce_xor_sync(0xffffffffu, v);
+            if (s == 0 && i < n) out[i] = (unsigned char)(all & 1);
+        }
+    }
+}
+
+template <int V, int UNR>
+static float run(const uint4 *blocks, u64 nblocks, const u64 *keys, u64 n, unsigned char *out,
+                 int reps) {
+    int sms = 0, per = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, gather<V, UNR>, 256, 0);
+    dim3 grid(sms * per);
+    gather<V, UNR><<<grid, 256>>>(blocks, nblocks, keys, n, out);
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    cudaEventRecord(a);
+    for (int r = 0; r < reps; ++r) gather<V, UNR><<<grid, 256>>>(blocks, nblocks, keys, n, out);
+    cudaEventRecord(b);
+    cudaEventSynchronize(b);
+    float ms = 0;
+    cudaEventElapsedTime(&ms, a, b);
+    return ms / reps;
+}
+
+__global__ void fill(u64 *p, u64 n) {
+    for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x)
+        p[i] = i * 0x9E3779B97F4A7C15ull;
+}
+
+int main(int argc, char **argv) {
+    const u64 mib = argc > 1 ? strtoull(argv[1], 0, 10) : 512;
+    const int lg = argc > 2 ? atoi(argv[2]) : 27;
+    const int only = argc > 3 ? atoi(argv[3]) : -1;
+    const u64 nblocks = mib * (1ull << 20) / 64, n = 1ull << lg;
+    uint4 *blocks;
+    u64 *keys;
+    unsigned char *out;
+    cudaMalloc(&blocks, nblocks * 64);
+    cudaMalloc(&keys, n * 8);
+    cudaMalloc(&out, n);
+    fill<<<1184, 256>>>((u64 *)blocks, nblocks * 8);
+    fill<<<1184, 256>>>(keys, n);
+    cudaDeviceSynchronize();
+    const double bytes = (double)n * (64 + 8 + 1);
+    const char *names[] = {"nc.L1::no_allocate", "cg", "nc.na.L2::64B", "nc.na.L2::128B",
+                           "nc.na.L2::256B"};
+    for (size_t gran : {0, 32, 64, 128}) {
+        if (gran) cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, gran);
+        size_t g = 0;
+        cudaDeviceGetLimit(&g, cudaLimitMaxL2FetchGranularity);
+        for (int v = 0; v < 5; ++v) {
+            if (only >= 0 && v != only) continue;
+            float ms1 = 0, ms2 = 0, ms4 = 0;
+            switch (v) {
+                case 0: ms1 = run<0, 1>(blocks, nblocks, keys, n, out, 5); ms2 = run<0, 2>(blocks, nblocks, keys, n, out, 5); ms4 = run<0, 4>(blocks, nblocks, keys, n, out, 5); break;
+                case 1: ms1 = run<1, 1>(blocks, nblocks, keys, n, out, 5); ms2 = run<1, 2>(blocks, nblocks, keys, n, out, 5); ms4 = run<1, 4>(blocks, nblocks, keys, n, out, 5); break;
+                case 2: ms1 = run<2, 1>(blocks, nblocks, keys, n, out, 5); ms2 = run<2, 2>(blocks, nblocks, keys, n, out, 5); ms4 = run<2, 4>(blocks, nblocks, keys, n, out, 5); break;
+                case 3: ms1 = run<3, 1>(blocks, nblocks, keys, n, out, 5); ms2 = run<3, 2>(blocks, nblocks, keys, n, out, 5); ms4 = run<3, 4>(blocks, nblocks, keys, n, out, 5); break;
+                case 4: ms1 = run<4, 1>(blocks, nblocks, keys, n, out, 5); ms2 = run<4, 2>(blocks, nblocks, keys, n, out, 5); ms4 = run<4, 4>(blocks, nblocks, keys, n, out, 5); break;
+            }
+            printf("filter %llu MiB  lookups 2^%d  gran %zu  %-20s  unr1 %.3f ms %.0f GB/s %.1f Gl/s | unr2 %.0f GB/s | unr4 %.0f GB/s\n",
+                   mib, lg, g, names[v], ms1, bytes / ms1 / 1e6, n / ms1 / 1e6, bytes / ms2 / 1e6,
+                   bytes / ms4 / 1e6);
+        }
+    }
+    cudaError_t e = cudaGetLastError();
+    printf("status: %s\n", cudaGetErrorString(e));
+    return e != cudaSuccess;
+}
