@@ -97,7 +97,10 @@ __global__ void fill(u64 *p, u64 n) {
         p[i] = i * 0x9E3779B97F4A7C15ull;
 }
 
+extern "C" int scatter_main(u64 mib, int lg);
+
 int main(int argc, char **argv) {
+    if (argc > 1 && argv[1][0] == 's') return scatter_main(strtoull(argv[2], 0, 10), atoi(argv[3]));
     const u64 mib = argc > 1 ? strtoull(argv[1], 0, 10) : 512;
     const int lg = argc > 2 ? atoi(argv[2]) : 27;
     const int only = argc > 3 ? atoi(argv[3]) : -1;
@@ -136,4 +139,63 @@ int main(int argc, char **argv) {
     cudaError_t e = cudaGetLastError();
     printf("status: %s\n", cudaGetErrorString(e));
     return e != cudaSuccess;
+}
+
+// ---- insert-side probe: random 64-byte-block OR updates ---------------------------
+// mode 0: 4 lanes x 2 RED.E.OR.64 per block; mode 1: plain ST.64 (racy, for
+// the write-back comparison only); mode 2: atom.or (returning)
+template <int MODE>
+__global__ void __launch_bounds__(256) scatter(u64 *__restrict__ words, u64 nblocks,
+                                               const u64 *__restrict__ keys, u64 n) {
+    const int s = threadIdx.x & 3;
+    const u64 g0 = (blockIdx.x * (u64)blockDim.x + threadIdx.x) >> 2;
+    const u64 groups = ((u64)gridDim.x * blockDim.x) >> 2;
+    for (u64 i = g0; i < n; i += groups) {
+        const u64 x = __ldcs(keys + i);
+        const u64 b = __umul64hi(mix(x), nblocks);
+        u64 *p = words + b * 8 + 2 * s;
+        const u64 v = mix(x + s) & mix(x ^ s);
+        if (MODE == 0) {
+            atomicOr((unsigned long long *)p, v);
+            atomicOr((unsigned long long *)p + 1, v >> 1);
+        } else if (MODE == 1) {
+            p[0] = v;
+            p[1] = v >> 1;
+        } else {
+            asm volatile("red.global.relaxed.gpu.or.b64 [%0], %1;" ::"l"(p), "l"(v));
+            asm volatile("red.global.relaxed.gpu.or.b64 [%0], %1;" ::"l"(p + 1), "l"(v >> 1));
+        }
+    }
+}
+
+extern "C" int scatter_main(u64 mib, int lg) {
+    const u64 nblocks = mib * (1ull << 20) / 64, n = 1ull << lg;
+    u64 *words, *keys;
+    cudaMalloc(&words, nblocks * 64);
+    cudaMalloc(&keys, n * 8);
+    fill<<<1184, 256>>>(keys, n);
+    cudaMemset(words, 0, nblocks * 64);
+    int sms = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    for (int mode = 0; mode < 3; ++mode) {
+        for (int rep = 0; rep < 3; ++rep) {
+            cudaEvent_t a, b;
+            cudaEventCreate(&a);
+            cudaEventCreate(&b);
+            cudaEventRecord(a);
+            if (mode == 0) scatter<0><<<sms * 8, 256>>>(words, nblocks, keys, n);
+            if (mode == 1) scatter<1><<<sms * 8, 256>>>(words, nblocks, keys, n);
+            if (mode == 2) scatter<2><<<sms * 8, 256>>>(words, nblocks, keys, n);
+            cudaEventRecord(b);
+            cudaEventSynchronize(b);
+            float ms = 0;
+            cudaEventElapsedTime(&ms, a, b);
+            if (rep == 2)
+                printf("scatter filter %llu MiB  2^%d updates  mode %d  %.3f ms  %.1f G/s\n", mib, lg,
+                       mode, ms, n / ms / 1e6);
+        }
+    }
+    cudaFree(words);
+    cudaFree(keys);
+    return 0;
 }
