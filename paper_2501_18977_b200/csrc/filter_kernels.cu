@@ -16,6 +16,7 @@
 #include <unordered_map>
 
 #include "blocks.cuh"
+#include "lookup.cuh"
 
 namespace cg = cooperative_groups;
 
@@ -83,6 +84,36 @@ __global__ void __launch_bounds__(kTPB) blocks512_kernel(const __grid_constant__
         __syncwarp();
     }
     if (OP == OP_CONTAINS && hits != nullptr) {
+        for (int o = 16; o > 0; o >>= 1) my_hits += __shfl_xor_sync(kFull, my_hits, o);
+        if (lane == 0 && my_hits) atomicAdd(hits, (unsigned long long)my_hits);
+    }
+}
+
+// Lookups, 512-bit blocks, random strategy: staged blocks + per-address test
+// (lookup.cuh), early exit over the choices.
+template <int C>
+__global__ void __launch_bounds__(kTPB) lookup512_kernel(const __grid_constant__ KParams p,
+                                                         const u64 *__restrict__ words,
+                                                         const u64 *__restrict__ keys, u64 n,
+                                                         u8 *__restrict__ out,
+                                                         unsigned long long *__restrict__ hits) {
+    __shared__ LookupSmem<C> smem[kWarps];
+    LookupSmem<C> &ls = smem[threadIdx.x >> 5];
+    const int lane = threadIdx.x & 31;
+    const u64 ntiles = (n + 31) / 32;
+    const u64 nwarps = (u64)gridDim.x * kWarps;
+    u32 my_hits = 0;
+    for (u64 tile = blockIdx.x * (u64)kWarps + (threadIdx.x >> 5); tile < ntiles;
+         tile += nwarps) {
+        const u64 base = tile * 32;
+        const bool valid = base + lane < n;
+        const u64 x = valid ? ld_stream(keys + base + lane) : 0ull;
+        const bool f = lookup_tile<C>(p, words, ls, x, valid, lane);
+        if (out != nullptr && valid) out[base + lane] = (u8)f;
+        my_hits += f ? 1u : 0u;
+        __syncwarp();
+    }
+    if (hits != nullptr) {
         for (int o = 16; o > 0; o >>= 1) my_hits += __shfl_xor_sync(kFull, my_hits, o);
         if (lane == 0 && my_hits) atomicAdd(hits, (unsigned long long)my_hits);
     }
@@ -259,6 +290,13 @@ __global__ void __launch_bounds__(256) eval_hash_kernel(DevHash h, const u64 *__
 template <int OP, int C>
 static cudaError_t launch512(const KParams &p, u64 *words, const u64 *keys, u64 n, u8 *out,
                              unsigned long long *hits, cudaStream_t s) {
+    if (OP == OP_CONTAINS && p.fast_random) {
+        const void *fl = (const void *)lookup512_kernel<C>;
+        const unsigned g = grid_for(fl, kTPB, 0, (n + kTPB - 1) / kTPB);
+        lookup512_kernel<C><<<g, kTPB, 0, s>>>(p, words, keys, n, out, hits);
+        count_launch();
+        return cudaGetLastError();
+    }
     const void *fn = (const void *)blocks512_kernel<OP, C>;
     const unsigned grid = grid_for(fn, kTPB, 0, (n + kTPB - 1) / kTPB);
     blocks512_kernel<OP, C><<<grid, kTPB, 0, s>>>(p, words, keys, n, out, hits);

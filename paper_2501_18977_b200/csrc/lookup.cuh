@@ -1,0 +1,75 @@
+// Lookup tile for 512-bit blocks and the random bit strategy
+// (contains_blocks, _kernels.py:177-211).
+//
+// A warp answers 32 keys per iteration:
+//
+//   1. one lane per key computes the c candidate block indices;
+//   2. per choice (in order): four lanes per pending key stage its 64-byte
+//      block into the warp's shared-memory slice with one LDG.128 + STS.128
+//      each (one L1 wavefront per block, conflict-free 128-bit stores);
+//   3. one lane per pending key tests its k bit addresses against the staged
+//      block -- a bit hash (3 IMAD) and one shared-memory word per address,
+//      no mask is materialised;
+//   4. keys found by this choice drop out; the next choice is only fetched
+//      for keys still pending, so a positive costs the blocks up to its first
+//      passing choice -- the reference's early exit (E[P] blocks, SURVEY
+//      §8(d)) rather than all c.
+#pragma once
+
+#include "common.cuh"
+
+namespace bc {
+
+template <int C>
+struct LookupSmem {
+    u32 blk[C][32];            // candidate block per choice and key
+    uint4 blocks[32][4];       // staged blocks, row r(kk), 16-byte quarters
+};
+
+// Row of key kk: keys 8q+p and 8q+4+p (one quarter-warp of STS.128) land in
+// different bank halves, so the staging stores are conflict-free.
+__device__ __forceinline__ int stage_row(int kk) { return kk ^ ((kk >> 2) & 1); }
+
+template <int C>
+__device__ __forceinline__ bool lookup_tile(const KParams &p, const u64 *__restrict__ words,
+                                            LookupSmem<C> &ls, u64 x, bool valid, int lane) {
+    constexpr u32 full = 0xffffffffu;
+#pragma unroll
+    for (int ci = 0; ci < C; ++ci) ls.blk[ci][lane] = valid ? (u32)block_index(p, x, ci) : 0u;
+    u32 done = __ballot_sync(full, !valid);
+    const u32 xlo = (u32)x, xhi = (u32)(x >> 32);
+    const int g = lane >> 2, s = lane & 3;
+    const uint4 *w4 = reinterpret_cast<const uint4 *>(words);
+    const u32 *mine = reinterpret_cast<const u32 *>(&ls.blocks[stage_row(lane)][0]);
+    bool found = false;
+#pragma unroll
+    for (int ci = 0; ci < C; ++ci) {
+        if (done == full) break;
+        __syncwarp();
+        uint4 w[4];
+#pragma unroll
+        for (int pp = 0; pp < 4; ++pp) {
+            const int kk = 4 * g + pp;
+            if (!((done >> kk) & 1u)) w[pp] = ld_block_cg(w4 + (u64)ls.blk[ci][kk] * 4 + s);
+        }
+#pragma unroll
+        for (int pp = 0; pp < 4; ++pp) {
+            const int kk = 4 * g + pp;
+            if (!((done >> kk) & 1u)) ls.blocks[stage_row(kk)][s] = w[pp];
+        }
+        __syncwarp();
+        if (!((done >> lane) & 1u)) {
+            u32 acc = 1u;
+#pragma unroll 4
+            for (u32 i = 0; i < p.k; ++i) {
+                const u32 h = bit512(p.bit_a_lo[i], p.bit_a_hi[i], xlo, xhi);
+                acc &= mine[h >> 5] >> (h & 31);
+            }
+            found = (acc & 1u) != 0u;
+        }
+        done |= __ballot_sync(full, found);
+    }
+    return found;
+}
+
+}  // namespace bc
