@@ -6,6 +6,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -254,6 +255,15 @@ static int ensure_ordered_scratch(bc_filter *f, cudaStream_t s) {
     return BC_OK;
 }
 
+// Region-partitioned single-choice inserts (partition_insert.cu) are opt-in:
+// on B200 the bucket scatter currently costs more than it saves (cfg2: 2.2 ms
+// vs 1.75 ms direct).  BC_PARTITION_MIN_KEYS=<n> enables them
+// for batches of at least n keys.
+static const u64 kPartitionMinKeys = []() -> u64 {
+    const char *e = std::getenv("BC_PARTITION_MIN_KEYS");
+    return e ? std::strtoull(e, nullptr, 10) : ~0ull;
+}();
+
 static int insert_device(bc_filter *f, u64 *words, const u64 *keys, u64 n, int mode,
                          cudaStream_t s) {
     if (n == 0) return BC_OK;
@@ -262,12 +272,33 @@ static int insert_device(bc_filter *f, u64 *words, const u64 *keys, u64 n, int m
         return BC_OK;
     }
     if (f->kp.c == 1) {  // OR commutes: any order is the reference's order
+        if (partition_supported(f->kp) && n >= kPartitionMinKeys) {
+            // region-partitioned: bucket by 64 KiB filter region, OR in shared memory
+            const u64 per = std::min<u64>(n, 1ull << 27);
+            void *scratch = nullptr;
+            CUDA_TRY(cudaMallocAsync(&scratch, partition_scratch_bytes(f->kp, per), s));
+            cudaError_t e = cudaSuccess;
+            for (u64 off = 0; off < n && e == cudaSuccess; off += per)
+                e = launch_partitioned_insert(f->kp, words, keys + off, std::min(per, n - off),
+                                              scratch, s);
+            cudaFreeAsync(scratch, s);
+            CUDA_TRY(e);
+            return BC_OK;
+        }
         CUDA_TRY(launch_blocks(OP_INSERT, f->kp, words, keys, n, nullptr, nullptr, s));
         return BC_OK;
     }
     if (mode == BC_INSERT_RELAXED) {
-        // keep at most M/2 keys in flight (FPR within ~3%)
+        // keep at most M/2 keys in flight (FPR within ~3%): one
+        // persistent launch whose grid holds <= M/2 keys (256 per CTA) at a time,
+        // or, for filters under 512 blocks, launches of M/2 keys each
         const u64 per = std::max<u64>(1, f->kp.num_blocks / 2);
+        if (per >= 256) {
+            KParams kp = f->kp;
+            kp.max_ctas = (u32)std::min<u64>(per / 256, 0xffffffffu);
+            CUDA_TRY(launch_blocks(OP_INSERT, kp, words, keys, n, nullptr, nullptr, s));
+            return BC_OK;
+        }
         for (u64 off = 0; off < n; off += per)
             CUDA_TRY(launch_blocks(OP_INSERT, f->kp, words, keys + off, std::min(per, n - off),
                                    nullptr, nullptr, s));

@@ -41,6 +41,7 @@ struct KParams {
     u64 flat_b, flat_magic;      // standard kind: range m = M*B
     u32 flat_mode, flat_shift;
     u32 k, c, wpb, strategy, block_bits, fast_random;
+    u32 max_ctas;                // launch cap (relaxed inserts: bounds keys in flight)
     const DevHash *bits;         // device, k entries
     const u32 *rank;             // device, (B+1)*(k+1) cost ranks (c >= 2)
     u32 bit_a_lo[kMaxFastK];     // fast_random: SHIFT 55 for every bit hash

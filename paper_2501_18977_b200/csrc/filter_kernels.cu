@@ -298,7 +298,8 @@ static cudaError_t launch512(const KParams &p, u64 *words, const u64 *keys, u64 
         return cudaGetLastError();
     }
     const void *fn = (const void *)blocks512_kernel<OP, C>;
-    const unsigned grid = grid_for(fn, kTPB, 0, (n + kTPB - 1) / kTPB);
+    unsigned grid = grid_for(fn, kTPB, 0, (n + kTPB - 1) / kTPB);
+    if (p.max_ctas && grid > p.max_ctas) grid = p.max_ctas;
     blocks512_kernel<OP, C><<<grid, kTPB, 0, s>>>(p, words, keys, n, out, hits);
     count_launch();
     return cudaGetLastError();
@@ -329,7 +330,8 @@ cudaError_t launch_blocks(int op, const KParams &p, u64 *words, const u64 *keys,
     }
     const void *fn = op == OP_CONTAINS ? (const void *)generic_kernel<OP_CONTAINS>
                                        : (const void *)generic_kernel<OP_INSERT>;
-    const unsigned grid = grid_for(fn, 256, 0, (n + 255) / 256);
+    unsigned grid = grid_for(fn, 256, 0, (n + 255) / 256);
+    if (p.max_ctas && grid > p.max_ctas) grid = p.max_ctas;
     if (op == OP_CONTAINS)
         generic_kernel<OP_CONTAINS><<<grid, 256, 0, s>>>(p, words, keys, n, out, hits);
     else

@@ -50,4 +50,14 @@ cudaError_t launch_qgram_blocks(int op, const KParams &p, u64 *words, const u8 *
                                 unsigned long long *hits, unsigned long long *count,
                                 cudaStream_t s);
 
+// In-place exclusive scan of n u64 by one CTA (*total = sum, nullable).
+cudaError_t launch_scan(u64 *v, u64 n, unsigned long long *total, cudaStream_t s);
+
+// ---- region-partitioned single-choice insert (partition_insert.cu) -----------------
+bool partition_supported(const KParams &p);
+u32 partition_regions(const KParams &p);
+size_t partition_scratch_bytes(const KParams &p, u64 n);
+cudaError_t launch_partitioned_insert(const KParams &p, u64 *words, const u64 *keys, u64 n,
+                                      void *scratch, cudaStream_t s);
+
 }  // namespace bc

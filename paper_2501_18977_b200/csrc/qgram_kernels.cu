@@ -203,6 +203,12 @@ __global__ void __launch_bounds__(kQgramThreads) qgram_blocks_kernel(
     }
 }
 
+cudaError_t launch_scan(u64 *v, u64 n, unsigned long long *total, cudaStream_t s) {
+    scan_kernel<<<1, 1024, 0, s>>>(v, n, total);
+    count_launch();
+    return cudaGetLastError();
+}
+
 // ---------------------------------------------------------------------------------
 static inline u64 n_windows(u64 len, int q) { return len >= (u64)q ? len - q + 1 : 0; }
 

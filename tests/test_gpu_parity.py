@@ -9,6 +9,7 @@
 """
 
 import hashlib
+import os
 
 import numpy as np
 import pytest
@@ -338,3 +339,24 @@ def test_fused_qgram_insert_single_choice_and_relaxed():
     g.insert_qgrams(enc, genome)
     assert g.contains_qgrams(enc, genome).all()
     assert g.count_qgram_hits(enc, genome) == keys.shape[0]
+
+
+def test_partitioned_single_choice_insert_bit_identical(golden, tmp_path):
+    """The opt-in region-partitioned insert (BC_PARTITION_MIN_KEYS) gives the
+    reference's bit array (run in a subprocess: the knob is read at load)."""
+    import subprocess
+    import sys
+
+    meta, _ = golden
+    case = meta["cfg2_small"]
+    script = (
+        "import hashlib, numpy as np, torch, paper_2501_18977_b200 as bb\n"
+        f"cfg = bb.FilterConfig(kind='blocked', k=12, size_bits=12 * 2**20, seed=1)\n"
+        "f = bb.Filter.from_config(cfg)\n"
+        f"f.insert_many(torch.from_numpy(bb.even_keys({case['n_insert']}, {case['insert_seed']})).cuda())\n"
+        "print(hashlib.sha256(f.storage.words.tobytes()).hexdigest())\n")
+    env = dict(os.environ, BC_PARTITION_MIN_KEYS="1")
+    out = subprocess.run([sys.executable, "-c", script], env=env, capture_output=True, text=True,
+                         cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    assert out.returncode == 0, out.stderr
+    assert out.stdout.strip().splitlines()[-1] == case["words_sha256"]

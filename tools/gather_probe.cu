@@ -161,9 +161,16 @@ __global__ void __launch_bounds__(256) scatter(u64 *__restrict__ words, u64 nblo
         } else if (MODE == 1) {
             p[0] = v;
             p[1] = v >> 1;
-        } else {
+        } else if (MODE == 2) {
             asm volatile("red.global.relaxed.gpu.or.b64 [%0], %1;" ::"l"(p), "l"(v));
             asm volatile("red.global.relaxed.gpu.or.b64 [%0], %1;" ::"l"(p + 1), "l"(v >> 1));
+        } else if (MODE == 3) {
+            // 8 lanes per block, one RED.64 each (same block = 2 sectors per 4 lanes)
+            u64 *q = words + b * 8 + (threadIdx.x & 7);
+            atomicOr((unsigned long long *)q, v);
+        } else {
+            // 4 lanes per block, one 32-byte sector pair... each lane 1 RED.64 at word 2s
+            atomicOr((unsigned long long *)p, v);
         }
     }
 }
@@ -177,7 +184,7 @@ extern "C" int scatter_main(u64 mib, int lg) {
     cudaMemset(words, 0, nblocks * 64);
     int sms = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
-    for (int mode = 0; mode < 3; ++mode) {
+    for (int mode = 0; mode < 5; ++mode) {
         for (int rep = 0; rep < 3; ++rep) {
             cudaEvent_t a, b;
             cudaEventCreate(&a);
@@ -186,6 +193,8 @@ extern "C" int scatter_main(u64 mib, int lg) {
             if (mode == 0) scatter<0><<<sms * 8, 256>>>(words, nblocks, keys, n);
             if (mode == 1) scatter<1><<<sms * 8, 256>>>(words, nblocks, keys, n);
             if (mode == 2) scatter<2><<<sms * 8, 256>>>(words, nblocks, keys, n);
+            if (mode == 3) scatter<3><<<sms * 8, 256>>>(words, nblocks, keys, n);
+            if (mode == 4) scatter<4><<<sms * 8, 256>>>(words, nblocks, keys, n);
             cudaEventRecord(b);
             cudaEventSynchronize(b);
             float ms = 0;
