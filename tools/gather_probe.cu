@@ -164,6 +164,12 @@ __global__ void __launch_bounds__(256) scatter(u64 *__restrict__ words, u64 nblo
         } else if (MODE == 2) {
             asm volatile("red.global.relaxed.gpu.or.b64 [%0], %1;" ::"l"(p), "l"(v));
             asm volatile("red.global.relaxed.gpu.or.b64 [%0], %1;" ::"l"(p + 1), "l"(v >> 1));
+        } else if (MODE == 5) {
+            // 8 lanes per key, one RED.64 per word: the whole 64-byte block in
+            // one instruction (keys of lanes 8h..8h+7 share the group's key)
+            const u64 xk = __shfl_sync(0xffffffffu, x, threadIdx.x & 24);
+            const u64 bk = __umul64hi(mix(xk), nblocks);
+            atomicOr((unsigned long long *)(words + bk * 8 + (threadIdx.x & 7)), mix(xk + s));
         } else if (MODE == 3) {
             // 8 lanes per block, one RED.64 each (same block = 2 sectors per 4 lanes)
             u64 *q = words + b * 8 + (threadIdx.x & 7);
@@ -184,7 +190,7 @@ extern "C" int scatter_main(u64 mib, int lg) {
     cudaMemset(words, 0, nblocks * 64);
     int sms = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
-    for (int mode = 0; mode < 5; ++mode) {
+    for (int mode = 0; mode < 6; ++mode) {
         for (int rep = 0; rep < 3; ++rep) {
             cudaEvent_t a, b;
             cudaEventCreate(&a);
@@ -195,6 +201,7 @@ extern "C" int scatter_main(u64 mib, int lg) {
             if (mode == 2) scatter<2><<<sms * 8, 256>>>(words, nblocks, keys, n);
             if (mode == 3) scatter<3><<<sms * 8, 256>>>(words, nblocks, keys, n);
             if (mode == 4) scatter<4><<<sms * 8, 256>>>(words, nblocks, keys, n);
+            if (mode == 5) scatter<5><<<sms * 8, 256>>>(words, nblocks, keys, n);
             cudaEventRecord(b);
             cudaEventSynchronize(b);
             float ms = 0;
