@@ -52,6 +52,11 @@ CONFIGS = {
                      "(50% pos, shuffled)",
             kind="blowchoc", c=3, k=16, n=2**28, bpk=16, nq=2**30, ref_keys=False,
             lookup_bytes=168.3),
+    4: dict(workload="cfg4: DNA, seeded i.i.d. 1.2e9-bp genome, canonical 31-mers into "
+                     "blowchoc c=2 k=14 at 14 b/key; lookups of 1e8 150-bp reads with 1% "
+                     "substitutions + 1e8 reads of an independent genome (count-only)",
+            kind="blowchoc", c=2, k=14, dna=True, genome=1_200_000_000, reads=10**8,
+            read_len=150, sub=0.01, q=31, ref_keys=False, lookup_bytes=117.0),
     5: dict(workload="cfg5: blowchoc c=2 k=11 8 GiB, 1.2*2^32 keys, 2^32 lookups per step "
                      "(50% pos)",
             kind="blowchoc", c=2, k=11, n=int(1.2 * 2**32), size_bits=2**36, nq=2**32,
@@ -73,6 +78,7 @@ def parse():
     ap.add_argument("--insert-mode", default=None, choices=["ordered", "relaxed"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--reads", type=int, default=None, help="config 4: reads per set")
     return ap.parse_args()
 
 
@@ -125,15 +131,24 @@ def make_inputs(cfg: dict, rank: int, device):
         return (torch.from_numpy(keys).to(device), torch.from_numpy(q).to(device),
                 torch.from_numpy(is_pos).to(device))
     g = torch.Generator(device=device).manual_seed(1234 + rank)
-    keys = torch.randint(-2**63, 2**63 - 1, (n,), device=device, dtype=torch.int64,
-                         generator=g) & ~1
-    # queries: low bit of a counter-hash picks positive (sample of keys) or negative (odd)
-    sel = torch.randint(0, 2, (nq,), device=device, dtype=torch.int64, generator=g).bool()
-    idx = torch.randint(0, n, (nq,), device=device, dtype=torch.int64, generator=g)
-    neg = torch.randint(-2**63, 2**63 - 1, (nq,), device=device, dtype=torch.int64,
-                        generator=g) | 1
-    q = torch.where(sel, keys[idx], neg)
-    del idx, neg
+    span = 1 << 28  # generate in slices: cfg5 holds 5e9 keys + 4e9 queries (~80 GB)
+    keys = torch.empty(n, dtype=torch.int64, device=device)
+    for a in range(0, n, span):
+        b = min(n, a + span)
+        keys[a:b] = torch.randint(-2**63, 2**63 - 1, (b - a,), device=device,
+                                  dtype=torch.int64, generator=g) & ~1
+    # queries: half uniform samples of the inserted keys, half odd (never inserted)
+    q = torch.empty(nq, dtype=torch.int64, device=device)
+    sel = torch.empty(nq, dtype=torch.bool, device=device)
+    for a in range(0, nq, span):
+        b = min(nq, a + span)
+        s = torch.randint(0, 2, (b - a,), device=device, dtype=torch.int64, generator=g).bool()
+        idx = torch.randint(0, n, (b - a,), device=device, dtype=torch.int64, generator=g)
+        neg = torch.randint(-2**63, 2**63 - 1, (b - a,), device=device, dtype=torch.int64,
+                            generator=g) | 1
+        q[a:b] = torch.where(s, keys[idx], neg)
+        sel[a:b] = s
+        del s, idx, neg
     return keys.view(torch.uint64), q.view(torch.uint64), sel
 
 
@@ -194,6 +209,15 @@ def measured_peak():
         return float(d["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs (measured copy)"
     except (OSError, KeyError, ValueError):
         return 6650.0, "fallback 6.65 TB/s (B200_PROFILING.md)"
+
+
+def random_ceiling(filter_bytes: int):
+    """Measured random 64-byte-gather ceiling (tools/gather_probe.cu, ld.global.cg,
+    profiles/r1/gather_probe_*.txt) for the nearest filter size, in algorithmic
+    GB/s of the lookup pattern (64 B block + 8 B key + 1 B answer)."""
+    table = [(96 << 20, 7011.0), (512 << 20, 3145.0), (2 << 30, 2551.0), (8 << 30, 2415.0)]
+    best = min(table, key=lambda t: abs(np.log2(t[0]) - np.log2(max(filter_bytes, 1))))
+    return best[1]
 
 
 def profiled_traffic(config: int, kernel: str):
@@ -320,7 +344,7 @@ def run_ours(args, cfg):
     dev = torch.device("cuda", torch.cuda.current_device())
     mode = args.insert_mode or ("relaxed" if cfg["c"] >= 2 else "ordered")
     fkw = dict(kind=cfg["kind"], k=cfg["k"], choices=cfg["c"], seed=1)
-    fkw["size_bits"] = cfg.get("size_bits", cfg["bpk"] * cfg["n"])
+    fkw["size_bits"] = cfg["size_bits"] if "size_bits" in cfg else cfg["bpk"] * cfg["n"]
     filt = bb.Filter.from_config(bb.FilterConfig(**fkw), insert_mode=mode)
     keys, queries, is_pos = make_inputs(cfg, rank, dev)
     out = torch.empty(queries.numel(), dtype=torch.uint8, device=dev)
@@ -407,9 +431,14 @@ def run_ours(args, cfg):
                 "frac": round(achieved / peak, 4), "traffic": traffic,
                 "kernel": f"{kname} ({klaunch} launch(es)/step, {kms:.3f} ms/step)",
                 "algorithmic_bytes_per_launch": kbytes / klaunch, "peak_source": peak_src}
-    if filt.storage.num_words * 8 < 126 * 2**20:
-        roofline["note"] = ("filter fits in L2 (126 MB): block traffic is served by L2, so "
+    if filt.storage.num_words * 8 <= 64 * 2**20:
+        roofline["note"] = ("filter mostly L2-resident: block traffic is served by L2, so "
                             "algorithmic GB/s can exceed the HBM copy peak")
+    elif filt.storage.num_words * 8 < 126 * 2**20:
+        roofline["note"] = ("filter below the 126 MB L2 size but not resident: ncu measures "
+                            "~43% L2 hits for lookups and dirty-line write-back for inserts "
+                            "(profiles/r1)")
+    roofline["random_sector_ceiling_gbs"] = random_ceiling(filt.storage.num_words * 8)
 
     line = {
         "metric": METRIC, "value": round(value, 2), "unit": "Mkeys/s", "n_gpus": world,
@@ -429,6 +458,8 @@ def run_ours(args, cfg):
         "roofline": roofline,
     }
 
+    if args.config == 5 and builder:
+        line["fpr_curve"] = fpr_curve(filt, keys, dev)
     # e2e through the public API from pinned host buffers
     if not args.no_e2e:
         line["e2e"] = run_e2e(args, cfg, filt, keys, queries, world, rank, dev)
@@ -487,11 +518,184 @@ def run_e2e(args, cfg, filt, keys, queries, world, rank, dev):
             "path": "Filter.insert_many/contains_many(pinned numpy) -> bc_*_host"}
 
 
+def fpr_curve(filt, keys, device, gammas=(0.2, 0.4, 0.6, 0.8, 1.0, 1.2), n_neg=1 << 26):
+    """FPR after inserting gamma x design capacity (cfg5: capacity 2^32 keys),
+    from n_neg odd keys; keys holds 1.2 x capacity in stream order."""
+    import torch
+
+    g = torch.Generator(device=device).manual_seed(77)
+    neg = (torch.randint(-2**63, 2**63 - 1, (n_neg,), device=device, dtype=torch.int64,
+                         generator=g) | 1).view(torch.uint64)
+    filt.storage.d_words.zero_()
+    cap = keys.numel() / 1.2
+    done, curve = 0, []
+    for gm in gammas:
+        upto = min(keys.numel(), int(round(gm * cap)))
+        if upto > done:
+            filt.insert_many(keys[done:upto])
+            done = upto
+        curve.append({"gamma": gm, "fpr": filt.count_hits(neg) / n_neg})
+    return curve
+
+
+def make_dna(cfg, device, n_reads):
+    """Genome, true reads (1% substitutions) and random reads, ASCII on the
+    device; reads are laid out 151 bytes apart (150 bases + '\\n')."""
+    import torch
+
+    L, R, RL = cfg["genome"], n_reads, cfg["read_len"]
+    g = torch.Generator(device=device).manual_seed(4)
+    lut = torch.tensor(list(b"ACGT"), dtype=torch.uint8, device=device)
+    codes = torch.empty(L, dtype=torch.uint8, device=device)
+    span = 1 << 27
+    for a in range(0, L, span):
+        b = min(L, a + span)
+        codes[a:b] = torch.randint(0, 4, (b - a,), device=device, dtype=torch.uint8, generator=g)
+    genome = torch.empty(L, dtype=torch.uint8, device=device)
+    for a in range(0, L, span):
+        b = min(L, a + span)
+        genome[a:b] = lut[codes[a:b].long()]
+    true_reads = torch.empty((R, RL + 1), dtype=torch.uint8, device=device)
+    rand_reads = torch.empty((R, RL + 1), dtype=torch.uint8, device=device)
+    true_reads[:, RL] = ord("\n")
+    rand_reads[:, RL] = ord("\n")
+    off = torch.arange(RL, device=device, dtype=torch.int64)
+    chunk = 1 << 20
+    for a in range(0, R, chunk):
+        b = min(R, a + chunk)
+        start = torch.randint(0, L - RL, (b - a, 1), device=device, dtype=torch.int64,
+                              generator=g)
+        c = codes[start + off]
+        sub = torch.rand((b - a, RL), device=device, generator=g) < cfg["sub"]
+        shift = torch.randint(1, 4, (b - a, RL), device=device, dtype=torch.uint8, generator=g)
+        c = torch.where(sub, (c + shift) % 4, c)
+        true_reads[a:b, :RL] = lut[c.long()]
+        rc = torch.randint(0, 4, (b - a, RL), device=device, dtype=torch.uint8, generator=g)
+        rand_reads[a:b, :RL] = lut[rc.long()]
+    del codes
+    return genome, true_reads.view(-1), rand_reads.view(-1)
+
+
+def run_dna(args, cfg):
+    """Config 4: fused q-gram insert of the genome, fused count-only lookups
+    of both read sets; value = k-mers processed per second."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_2501_18977_b200 as bb
+    from paper_2501_18977_b200 import _native
+
+    world, rank, local = dist_env()
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(0)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    mode = args.insert_mode or "relaxed"
+    q = cfg["q"]
+    L = cfg["genome"]
+    R = args.reads or cfg["reads"]
+    RL = cfg["read_len"]
+    filt = bb.Filter.from_config(bb.FilterConfig(kind="blowchoc", k=cfg["k"], choices=cfg["c"],
+                                                 size_bits=cfg["k"] * (L - q + 1), seed=1),
+                                 insert_mode=mode)
+    enc = bb.QGramEncoder(q, True)
+    genome, true_reads, rand_reads = make_dna(cfg, dev, R)
+    words = filt.storage.d_words
+    stream = torch.cuda.current_stream()
+    builder = rank == 0
+    res = {}
+
+    def step(ev):
+        ev[0].record(stream)
+        if builder:
+            words.zero_()
+            res["inserted"] = filt.insert_qgrams(enc, genome)
+        ev[1].record(stream)
+        if world > 1:
+            dist.broadcast(words, src=0)
+        ev[2].record(stream)
+        res["hits_true"] = filt.count_qgram_hits(enc, true_reads)
+        res["hits_rand"] = filt.count_qgram_hits(enc, rand_reads)
+        ev[3].record(stream)
+
+    events = [[torch.cuda.Event(enable_timing=True) for _ in range(4)]
+              for _ in range(args.warmup + args.steps)]
+    sampler = ClockSampler(torch.cuda.current_device())
+    sampler.start()
+    for i in range(args.warmup):
+        step(events[i])
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    l0 = _native.launch_count()
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0.record(stream)
+    for i in range(args.warmup, args.warmup + args.steps):
+        step(events[i])
+    t1.record(stream)
+    torch.cuda.synchronize()
+    launches = _native.launch_count() - l0
+    clocks = sampler.stop()
+    elapsed = t0.elapsed_time(t1)
+    if world > 1:
+        t = torch.tensor([elapsed], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        elapsed = float(t.item())
+    timed = events[args.warmup:]
+    ins_ms = sum(e[0].elapsed_time(e[1]) for e in timed) / args.steps
+    look_ms = sum(e[2].elapsed_time(e[3]) for e in timed) / args.steps
+    ms = elapsed / args.steps
+    win_read = RL - q + 1
+    kmers_ins = L - q + 1
+    kmers_look = 2 * R * win_read
+    value = (kmers_ins + world * kmers_look) / (ms / 1e3) / 1e6
+    peak, peak_src = measured_peak()
+    look_bytes = cfg["lookup_bytes"] * kmers_look + 2 * R * (RL + 1)
+    ins_bytes = insert_bytes(cfg["c"]) * kmers_ins + L
+    if look_ms >= ins_ms:
+        kname, kms, kbytes = "contains_qgrams", look_ms, look_bytes
+    else:
+        kname, kms, kbytes = "insert_qgrams", ins_ms, ins_bytes
+    achieved = kbytes / (kms / 1e3) / 1e9
+    line = {
+        "metric": METRIC, "value": round(value, 2), "unit": "Mk-mers/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 3),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64",
+        "data": "synthetic: seeded i.i.d. ACGT genome and reads generated on the device",
+        "config": {"workload": cfg["workload"] + (f" [reads={R}]" if R != cfg["reads"] else ""),
+                   "insert_mode": mode, "l2": "inputs larger than L2"},
+        "insert_mkmers_s": round(kmers_ins / ins_ms / 1e3, 2),
+        "lookup_mkmers_s": round(kmers_look / look_ms / 1e3, 2),
+        "inserted_kmers": res["inserted"],
+        "true_read_kmer_hit_rate": res["hits_true"] / (R * win_read),
+        "expected_true_rate_approx": 0.99 ** q,
+        "fpr": res["hits_rand"] / (R * win_read),
+        "gpu_launches": int(launches), "clocks": clocks,
+        "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
+                     "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": None,
+                     "kernel": f"{kname} ({kms:.2f} ms/step)", "peak_source": peak_src},
+        "e2e": {"value": None, "unit": "Mk-mers/s",
+                "note": "DNA inputs are generated on the device; see configs 1-2 for e2e"},
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
 def main():
     args = parse()
     cfg = CONFIGS[args.config]
     if args.impl == "reference":
+        if cfg.get("dna"):
+            print(json.dumps({"impl": "reference", "unavailable":
+                              "config 4 reference arm not wired (use configs 1-3, 5)"}))
+            return
         run_reference(args, cfg)
+    elif cfg.get("dna"):
+        run_dna(args, cfg)
     else:
         run_ours(args, cfg)
 

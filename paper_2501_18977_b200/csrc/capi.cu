@@ -242,7 +242,10 @@ static int check_device(bc_filter *f) {
 static int ensure_ordered_scratch(bc_filter *f, cudaStream_t s) {
     if (f->d_owner) return BC_OK;
     const u64 M = f->kp.num_blocks;
-    u64 chunk = M / 8;
+    // M/8-key chunks need ~8 claim rounds and ~1.25 visits per key; small
+    // filters are bound by the per-round grid syncs instead, so they take
+    // M/2-key chunks (~12 rounds, ~2 visits per key) -- SURVEY App. B
+    u64 chunk = M < (1ull << 20) ? M / 2 : M / 8;
     chunk = std::max<u64>(chunk, 256);
     chunk = std::min<u64>(chunk, 1ull << 24);
     CUDA_TRY(cudaMalloc(&f->d_owner, sizeof(u64) * M));
