@@ -297,9 +297,66 @@ def cpu_rate(cfg: dict, words_host: np.ndarray | None) -> dict:
     return r
 
 
+def cpu_dna_rate(cfg: dict) -> dict:
+    """Oracle k-mers/s for config 4 on a bounded sample: encode + insert a
+    4 Mbp genome prefix (one writer, stream order), then encode + look up
+    2 x 40 000 reads (joined with separators, all host threads); the rate is
+    weighted to the step's mix of inserted and looked-up k-mers."""
+    from oracle import oracle as orc
+
+    threads = host_cores()
+    q, RL = cfg["q"], cfg["read_len"]
+    rng = np.random.default_rng(4)
+    Lp, R = 4_000_000, 40_000
+    alphabet = np.frombuffer(b"ACGT", dtype=np.uint8)
+    codes = rng.integers(0, 4, Lp)
+    genome = alphabet[codes].tobytes()
+    t0 = time.perf_counter()
+    keys = orc.encode_qgrams(genome, q, True)
+    f = orc.make_filter("blowchoc", k=cfg["k"], choices=cfg["c"], seed=1,
+                        size_bits=cfg["k"] * (Lp - q + 1))
+    f.insert_many(keys)
+    t_ins = time.perf_counter() - t0
+    starts = rng.integers(0, Lp - RL, R)
+    reads = codes[starts[:, None] + np.arange(RL)]
+    sub = rng.random(reads.shape) < cfg["sub"]
+    reads = np.where(sub, (reads + rng.integers(1, 4, reads.shape)) % 4, reads)
+    rand = rng.integers(0, 4, (R, RL))
+    sep = np.full((R, 1), ord("\n"), dtype=np.uint8)
+    blob = np.concatenate([np.concatenate([alphabet[reads], sep], 1).ravel(),
+                           np.concatenate([alphabet[rand], sep], 1).ravel()]).tobytes()
+    t0 = time.perf_counter()
+    qk = orc.encode_qgrams(blob, q, True)
+    f.contains_many(qk, threads=threads)
+    t_look = time.perf_counter() - t0
+    ins_rate, look_rate = keys.shape[0] / t_ins, qk.shape[0] / t_look
+    n_ins = cfg["genome"] - q + 1
+    n_look = 2 * cfg["reads"] * (RL - q + 1)
+    value = (n_ins + n_look) / (n_ins / ins_rate + n_look / look_rate) / 1e6
+    return dict(value=round(value, 3), unit="Mk-mers/s", cores=threads, kind="port",
+                sample=(f"encode+insert of a {Lp}-bp genome prefix (1 writer) + encode+lookup "
+                        f"of 2x{R} reads ({threads} threads); rate weighted to the step's "
+                        f"{n_ins} inserted + {n_look} looked-up k-mers"),
+                insert_mkmers_s=round(ins_rate / 1e6, 3),
+                lookup_mkmers_s=round(look_rate / 1e6, 3), cpu=cpu_model())
+
+
 def run_reference(args, cfg):
     world, rank, _ = dist_env()
     if rank != 0:
+        return
+    if cfg.get("dna"):
+        vals = [cpu_dna_rate(cfg) for _ in range(args.warmup + args.steps)][args.warmup:]
+        r = vals[-1]
+        value = statistics.median(v["value"] for v in vals)
+        print(json.dumps({
+            "impl": "reference", "metric": METRIC, "value": value, "unit": "Mk-mers/s",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64",
+            "data": "synthetic i.i.d. genome and reads", "config": {"workload": cfg["workload"]},
+            "cpu_baseline": dict(r, value=value),
+            "e2e": {"value": value, "unit": "Mk-mers/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}), flush=True)
         return
     f, built = oracle_filter(cfg, None)
     vals = []
@@ -679,6 +736,8 @@ def run_dna(args, cfg):
         "e2e": {"value": None, "unit": "Mk-mers/s",
                 "note": "DNA inputs are generated on the device; see configs 1-2 for e2e"},
     }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_dna_rate(cfg)
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -689,10 +748,6 @@ def main():
     args = parse()
     cfg = CONFIGS[args.config]
     if args.impl == "reference":
-        if cfg.get("dna"):
-            print(json.dumps({"impl": "reference", "unavailable":
-                              "config 4 reference arm not wired (use configs 1-3, 5)"}))
-            return
         run_reference(args, cfg)
     elif cfg.get("dna"):
         run_dna(args, cfg)

@@ -227,38 +227,27 @@ u64 orc_encode_qgrams(const uint8_t *seq, u64 len, int q, int canonical, u64 *ou
     if (len < (u64)q)
         return 0;
     u64 qmask = q == 32 ? ~(u64)0 : (((u64)1 << (2 * q)) - 1);
-    u64 cnt = 0;
-    for (u64 i = 0; i + (u64)q <= len; ++i) {
-        u64 code = 0;
-        int ok = 1;
-        for (int t = 0; t < q; ++t) {
-            uint8_t ch = seq[i + (u64)t];
-            int v;
-            switch (ch) {
-            case 'A': case 'a': v = 0; break;
-            case 'C': case 'c': v = 1; break;
-            case 'G': case 'g': v = 2; break;
-            case 'T': case 't': v = 3; break;
-            default: v = -1;
-            }
-            if (v < 0) {
-                ok = 0;
-                break;
-            }
-            code = (code << 2) | (u64)v;
+    u64 cnt = 0, code = 0, rc = 0;
+    int run = 0; /* valid bases ending at position i */
+    for (u64 i = 0; i < len; ++i) {
+        int v;
+        switch (seq[i]) {
+        case 'A': case 'a': v = 0; break;
+        case 'C': case 'c': v = 1; break;
+        case 'G': case 'g': v = 2; break;
+        case 'T': case 't': v = 3; break;
+        default: v = -1;
         }
-        if (!ok)
+        if (v < 0) {
+            run = 0;
             continue;
-        if (canonical) {
-            u64 comp = code ^ qmask, rc = 0;
-            for (int t = 0; t < q; ++t) {
-                rc = (rc << 2) | (comp & 3);
-                comp >>= 2;
-            }
-            if (rc < code)
-                code = rc;
         }
-        out[cnt++] = code;
+        code = ((code << 2) | (u64)v) & qmask; /* first base most significant */
+        /* reverse complement: complement of the newest base enters on top */
+        rc = (rc >> 2) | ((u64)(3 - v) << (2 * q - 2));
+        if (++run < q)
+            continue;
+        out[cnt++] = (canonical && rc < code) ? rc : code;
     }
     return cnt;
 }
