@@ -130,12 +130,17 @@ __device__ __forceinline__ u32 phase2(const KParams &p, u64 *words, WarpSmem<C> 
     constexpr int CL = kNoLoad ? 1 : C;
     const int g = lane >> 2, s = lane & 3;
     const uint4 *w4 = reinterpret_cast<const uint4 *>(words);
+    // Lane s holds 64-bit mask words {2s, 2s+1} (matching its 16-byte slice of
+    // a loaded block), or -- for single-choice inserts, which load nothing --
+    // words {s, s+4}, so each of the two RED instructions of a group stays
+    // inside one 32-byte sector (tools/gather_probe.cu scatter mode 6 vs 0).
+    const int w0 = kNoLoad ? 2 * s : 4 * s, w2 = kNoLoad ? 2 * s + 8 : 4 * s + 2;
     uint4 M[4];
 #pragma unroll
     for (int r = 0; r < 4; ++r) {
         const int kr = 4 * g + ((r + s) & 3);
-        M[r] = make_uint4(ws.mask[4 * s][kr], ws.mask[4 * s + 1][kr], ws.mask[4 * s + 2][kr],
-                          ws.mask[4 * s + 3][kr]);
+        M[r] = make_uint4(ws.mask[w0][kr], ws.mask[w0 + 1][kr], ws.mask[w2][kr],
+                          ws.mask[w2 + 1][kr]);
     }
     u32 found_bytes = 0;
 #pragma unroll
@@ -168,9 +173,9 @@ __device__ __forceinline__ u32 phase2(const KParams &p, u64 *words, WarpSmem<C> 
                 }
                 found_bytes |= (found ? 1u : 0u) << (8 * pass);
             } else if (C == 1) {
-                u64 *dst = words + (u64)ws.blk[0][kk] * 8 + 2 * s;
+                u64 *dst = words + (u64)ws.blk[0][kk] * 8 + s;
                 red_or(dst, lo);
-                red_or(dst + 1, hi);
+                red_or(dst + 4, hi);
             } else {
                 u32 v[CL];
 #pragma unroll

@@ -164,6 +164,11 @@ __global__ void __launch_bounds__(256) scatter(u64 *__restrict__ words, u64 nblo
         } else if (MODE == 2) {
             asm volatile("red.global.relaxed.gpu.or.b64 [%0], %1;" ::"l"(p), "l"(v));
             asm volatile("red.global.relaxed.gpu.or.b64 [%0], %1;" ::"l"(p + 1), "l"(v >> 1));
+        } else if (MODE == 6) {
+            // 4 lanes x 2 RED.64, each instruction on one 32-byte sector
+            u64 *q = words + b * 8 + s;
+            atomicOr((unsigned long long *)q, v);
+            atomicOr((unsigned long long *)(q + 4), v >> 1);
         } else if (MODE == 5) {
             // 8 lanes per key, one RED.64 per word: the whole 64-byte block in
             // one instruction (keys of lanes 8h..8h+7 share the group's key)
@@ -190,7 +195,7 @@ extern "C" int scatter_main(u64 mib, int lg) {
     cudaMemset(words, 0, nblocks * 64);
     int sms = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
-    for (int mode = 0; mode < 6; ++mode) {
+    for (int mode = 0; mode < 7; ++mode) {
         for (int rep = 0; rep < 3; ++rep) {
             cudaEvent_t a, b;
             cudaEventCreate(&a);
@@ -202,6 +207,7 @@ extern "C" int scatter_main(u64 mib, int lg) {
             if (mode == 3) scatter<3><<<sms * 8, 256>>>(words, nblocks, keys, n);
             if (mode == 4) scatter<4><<<sms * 8, 256>>>(words, nblocks, keys, n);
             if (mode == 5) scatter<5><<<sms * 8, 256>>>(words, nblocks, keys, n);
+            if (mode == 6) scatter<6><<<sms * 8, 256>>>(words, nblocks, keys, n);
             cudaEventRecord(b);
             cudaEventSynchronize(b);
             float ms = 0;
