@@ -1,0 +1,222 @@
+"""Filter files (BWCH v1) and key input streams (reference io.py:1-121, 182-267).
+
+The file format is the reference's, byte for byte (pinned by the reference's
+test_io.py:70-86 and by tests/test_io_format.py here):
+
+    0  4s  magic "BWCH"          24 Q  block width in bits
+    4  I   version (1)           32 Q  number of blocks
+    8  B   kind 0/1/2            40 Q  shard count
+    9  H   k                     48 Q  seed
+    11 B   choices               56 Q  keys inserted
+    12 B   strategy 0/1          64 ... bit array: blocks in order, 64-bit
+    13 B   cost kind 0/1/2               little-endian words, LSB first
+    14 2x  reserved
+    16 d   cost parameter
+
+Filters live in HBM; ``write_filter`` streams the device words to the file in
+slices and ``read_filter`` streams them back, so multi-GiB filters never need
+a second full host copy.  Hash functions are re-derived from the stored seed.
+"""
+
+from __future__ import annotations
+
+import struct
+import sys
+from typing import BinaryIO, Iterator
+
+import numpy as np
+
+from .filters import CostModel, Filter
+from .qgrams import QGramEncoder, encode_qgrams
+
+MAGIC = b"BWCH"
+FORMAT_VERSION = 1
+HEADER = struct.Struct("<4sIBHBBB2xdQQQQQ")
+assert HEADER.size == 64
+
+KIND_CODES = {"standard": 0, "blocked": 1, "blowchoc": 2}
+STRATEGY_CODES = {"random": 0, "distinct": 1}
+COST_CODES = {"exp": 0, "mix": 1, "la": 2}
+KEY_FORMATS = ("u64le", "text", "fasta")
+
+_SLICE_WORDS = 1 << 24  # 128 MiB per device<->file transfer
+
+
+class FilterFormatError(Exception):
+    """The file is not a valid filter of a supported version."""
+
+
+class KeyFormatError(Exception):
+    """A key input stream could not be decoded."""
+
+
+def _inverse(d: dict) -> dict:
+    return {v: k for k, v in d.items()}
+
+
+def write_filter(filt: Filter, path) -> None:
+    if filt.block_bits % 64 != 0:
+        raise ValueError("only word-multiple block widths serialize")
+    code, param = (COST_CODES[filt.cost.kind], float(filt.cost.param)) if filt.cost else (0, 0.0)
+    header = HEADER.pack(MAGIC, FORMAT_VERSION, KIND_CODES[filt.kind], filt.k, filt.choices,
+                         STRATEGY_CODES[filt.strategy], code, param, filt.block_bits,
+                         filt.num_blocks, filt.shards, filt.seed, filt.inserted)
+    st = filt.storage
+    with open(path, "wb") as fh:
+        fh.write(header)
+        if st._d_words is None or st._host_valid:
+            fh.write(np.ascontiguousarray(st.words, dtype="<u8").tobytes())
+            return
+        d = st.d_words
+        for a in range(0, st.num_words, _SLICE_WORDS):
+            b = min(st.num_words, a + _SLICE_WORDS)
+            fh.write(d[a:b].cpu().numpy().astype("<u8", copy=False).tobytes())
+
+
+def _check_header(fields) -> tuple:
+    (magic, version, kind_code, k, choices, strategy_code, cost_code, cost_param,
+     block_bits, num_blocks, shards, seed, inserted) = fields
+    if magic != MAGIC:
+        raise FilterFormatError(f"bad magic {magic!r}")
+    if version != FORMAT_VERSION:
+        raise FilterFormatError(f"unsupported format version {version}")
+    kinds, strategies, costs = _inverse(KIND_CODES), _inverse(STRATEGY_CODES), _inverse(COST_CODES)
+    if kind_code not in kinds or strategy_code not in strategies or cost_code not in costs:
+        raise FilterFormatError("unknown enum value in header")
+    if (block_bits == 0 or block_bits % 64 or num_blocks == 0 or shards == 0
+            or num_blocks % shards or not 1 <= k <= block_bits):
+        raise FilterFormatError("inconsistent filter geometry")
+    kind = kinds[kind_code]
+    ok = {"standard": choices == 0, "blocked": choices == 1,
+          "blowchoc": 2 <= choices <= 8}[kind]
+    if not ok:
+        raise FilterFormatError(f"{kind} filter with {choices} choices")
+    if kind == "standard" and shards != 1:
+        raise FilterFormatError("standard filters do not shard")
+    cost = CostModel(costs[cost_code], cost_param, k) if kind == "blowchoc" else None
+    return (kind, k, choices, strategies[strategy_code], cost, block_bits, num_blocks, shards,
+            seed, inserted)
+
+
+def read_filter(path, **kw) -> Filter:
+    with open(path, "rb") as fh:
+        raw = fh.read(HEADER.size)
+        if len(raw) < HEADER.size:
+            raise FilterFormatError("truncated header")
+        (kind, k, choices, strategy, cost, block_bits, num_blocks, shards, seed,
+         inserted) = _check_header(HEADER.unpack(raw))
+        nbytes = num_blocks * block_bits // 8
+        try:
+            filt = Filter(kind=kind, k=k, choices=choices, strategy=strategy, cost=cost,
+                          block_bits=block_bits, num_blocks=num_blocks, shards=shards,
+                          seed=seed, inserted=inserted, **kw)
+        except ValueError as exc:
+            raise FilterFormatError(str(exc)) from exc
+        st = filt.storage
+        import torch
+
+        on_device = torch.cuda.is_available()
+        host = None if on_device else np.empty(st.num_words, dtype=np.uint64)
+        got = 0
+        for a in range(0, st.num_words, _SLICE_WORDS):
+            b = min(st.num_words, a + _SLICE_WORDS)
+            chunk = fh.read((b - a) * 8)
+            got += len(chunk)
+            if len(chunk) != (b - a) * 8:
+                raise FilterFormatError(f"bit array has {got} bytes, expected {nbytes}")
+            words = np.frombuffer(chunk, dtype="<u8").astype(np.uint64)
+            if on_device:
+                st.d_words[a:b].copy_(torch.from_numpy(words))
+            else:
+                host[a:b] = words
+        if fh.read(1):
+            raise FilterFormatError(f"bit array has more than {nbytes} bytes, expected {nbytes}")
+    if on_device:
+        st.device_modified()
+    else:
+        st.load_words(host)
+    return filt
+
+
+# -- key streams -----------------------------------------------------------------------
+
+def _open_binary(path) -> BinaryIO:
+    return sys.stdin.buffer if path == "-" else open(path, "rb")
+
+
+def _read_u64le(fh: BinaryIO, chunk: int) -> Iterator[np.ndarray]:
+    tail = b""
+    while True:
+        data = fh.read(chunk * 8)
+        if not data:
+            break
+        data = tail + data
+        cut = len(data) - len(data) % 8
+        if cut:
+            yield np.frombuffer(data[:cut], dtype="<u8").astype(np.uint64)
+        tail = data[cut:]
+    if tail:
+        raise KeyFormatError(f"u64le stream truncated ({len(tail)} stray bytes)")
+
+
+def _read_text(fh: BinaryIO, chunk: int) -> Iterator[np.ndarray]:
+    batch: list = []
+    for lineno, line in enumerate(fh, start=1):
+        line = line.strip()
+        if not line:
+            continue
+        try:
+            v = int(line)
+        except ValueError as exc:
+            raise KeyFormatError(f"line {lineno}: not an integer: {line!r}") from exc
+        if not 0 <= v < 2**64:
+            raise KeyFormatError(f"line {lineno}: key out of 64-bit range: {v}")
+        batch.append(v)
+        if len(batch) >= chunk:
+            yield np.array(batch, dtype=np.uint64)
+            batch = []
+    if batch:
+        yield np.array(batch, dtype=np.uint64)
+
+
+def fasta_records(fh: BinaryIO) -> Iterator[bytes]:
+    """Sequence of each FASTA record (lines joined, header dropped)."""
+    parts: list = []
+    seen = False
+    for line in fh:
+        line = line.strip()
+        if line.startswith(b">"):
+            if parts:
+                yield b"".join(parts)
+                parts = []
+            seen = True
+        elif line:
+            if not seen:
+                raise KeyFormatError("FASTA input does not start with a header line")
+            parts.append(line)
+    if parts:
+        yield b"".join(parts)
+
+
+def read_keys(path, fmt: str, *, q: int | None = None, canonical: bool = True,
+              chunk_size: int = 1 << 20) -> Iterator[np.ndarray]:
+    """Key chunks from a file ('-' = stdin): raw u64le, decimal text, or the
+    q-grams of each FASTA record (encoded on the GPU)."""
+    if fmt not in KEY_FORMATS:
+        raise KeyFormatError(f"unknown key format {fmt!r}")
+    if fmt == "fasta":
+        if q is None:
+            raise KeyFormatError("FASTA input needs a q-gram length")
+        enc = QGramEncoder(q=q, canonical=canonical)
+    fh = _open_binary(path)
+    try:
+        if fmt == "u64le":
+            yield from _read_u64le(fh, chunk_size)
+        elif fmt == "text":
+            yield from _read_text(fh, chunk_size)
+        else:
+            for rec in fasta_records(fh):
+                yield encode_qgrams(enc, rec)
+    finally:
+        if fh is not sys.stdin.buffer:
+            fh.close()

@@ -255,7 +255,40 @@ def dna_case(store: dict, meta: dict) -> None:
                        read_hits=hits, reads_sha256=hashlib.sha256(b"".join(reads)).hexdigest())
 
 
+def bwch_files() -> None:
+    """BWCH v1 files written by the reference's write_filter (io.py:60-72)."""
+    from blowchoc import write_filter
+
+    out = os.path.join(OUT, "bwch")
+    os.makedirs(out, exist_ok=True)
+    cases = {
+        "blocked_pinned": (FilterConfig(kind="blocked", k=4, size_bits=2 * 512, seed=0x1234),
+                           None),
+        "blowchoc_mix": (FilterConfig(kind="blowchoc", k=6, n_capacity=300, choices=3,
+                                      cost=CostModel("mix", 2.5, 6), seed=99, shards=2), 300),
+        "standard": (FilterConfig(kind="standard", k=5, n_capacity=200, seed=5,
+                                  block_bits=128), 200),
+        "distinct": (FilterConfig(kind="blowchoc", k=7, n_capacity=250, choices=2,
+                                  strategy="distinct", seed=3, block_bits=64), 250),
+    }
+    meta = {}
+    for name, (cfg, n) in cases.items():
+        f = Filter.from_config(cfg)
+        if n is None:  # the reference's own pinned-layout case (test_io.py:70-86)
+            f.storage.set_bits(0, {0, 1})
+            f.storage.set_bits(1, {64})
+        else:
+            f.insert_many(even_keys(n, 8))
+        p = os.path.join(out, name + ".bwch")
+        write_filter(f, p)
+        with open(p, "rb") as fh:
+            meta[name] = dict(n=n, sha256=hashlib.sha256(fh.read()).hexdigest())
+    with open(os.path.join(out, "index.json"), "w") as fh:
+        json.dump(meta, fh, indent=1)
+
+
 def main() -> None:
+    bwch_files()
     store: dict = {}
     meta: dict = {}
     hash_kats(store)

@@ -1,0 +1,161 @@
+"""BWCH v1 filter files and key streams (reference io.py; test_io.py:38-151).
+
+CPU tests read and re-write files produced by the reference itself
+(tests/golden/bwch, made by tests/golden/make_golden.py) and pin the byte
+layout; the GPU test round-trips a GPU-built filter."""
+
+import hashlib
+import json
+import os
+
+import numpy as np
+import pytest
+
+import paper_2501_18977_b200 as bb
+from paper_2501_18977_b200.io import (FilterFormatError, KeyFormatError, read_filter,
+                                      read_keys, write_filter)
+
+GOLD = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "bwch")
+
+
+def index():
+    with open(os.path.join(GOLD, "index.json")) as fh:
+        return json.load(fh)
+
+
+@pytest.mark.parametrize("name", ["blocked_pinned", "blowchoc_mix", "standard", "distinct"])
+def test_reference_files_roundtrip_bytes(name, tmp_path, monkeypatch):
+    """Read a reference-written file and write it back: identical bytes."""
+    import torch
+
+    monkeypatch.setattr(torch.cuda, "is_available", lambda: False)  # host path
+    src = os.path.join(GOLD, name + ".bwch")
+    f = read_filter(src)
+    dst = tmp_path / "out.bwch"
+    write_filter(f, dst)
+    raw = dst.read_bytes()
+    assert hashlib.sha256(raw).hexdigest() == index()[name]["sha256"]
+    assert raw == open(src, "rb").read()
+
+
+def test_file_layout_is_pinned(tmp_path):
+    filt = bb.Filter.from_config(bb.FilterConfig(kind="blocked", k=4, size_bits=2 * 512,
+                                                 seed=0x1234))
+    filt.storage.set_bits(0, {0, 1})
+    filt.storage.set_bits(1, {64})
+    p = tmp_path / "f"
+    write_filter(filt, p)
+    raw = p.read_bytes()
+    assert len(raw) == 64 + 2 * 64
+    assert raw[:4] == b"BWCH"
+    assert raw[4:8] == (1).to_bytes(4, "little")
+    assert raw[8] == 1
+    assert raw[9:11] == (4).to_bytes(2, "little")
+    assert raw[24:32] == (512).to_bytes(8, "little")
+    assert raw[48:56] == (0x1234).to_bytes(8, "little")
+    assert raw[64:72] == (0b11).to_bytes(8, "little")
+    assert raw[128 + 8:128 + 16] == (1).to_bytes(8, "little")
+    assert raw == open(os.path.join(GOLD, "blocked_pinned.bwch"), "rb").read()
+
+
+def _mutated(tmp_path, offset, value, name="blocked_pinned"):
+    raw = bytearray(open(os.path.join(GOLD, name + ".bwch"), "rb").read())
+    raw[offset] = value
+    p = tmp_path / "bad"
+    p.write_bytes(bytes(raw))
+    return p
+
+
+def test_rejects_corrupt_headers(tmp_path):
+    with pytest.raises(FilterFormatError, match="magic"):
+        read_filter(_mutated(tmp_path, 0, ord("X")))
+    with pytest.raises(FilterFormatError, match="version"):
+        read_filter(_mutated(tmp_path, 4, 99))
+    with pytest.raises(FilterFormatError, match="shard"):
+        read_filter(_mutated(tmp_path, 40, 2, "standard"))
+    with pytest.raises(FilterFormatError, match="choices"):
+        read_filter(_mutated(tmp_path, 11, 0, "blowchoc_mix"))
+    with pytest.raises(FilterFormatError, match="enum"):
+        read_filter(_mutated(tmp_path, 8, 7))
+    p = tmp_path / "short"
+    p.write_bytes(b"BWCH" + b"\x00" * 10)
+    with pytest.raises(FilterFormatError, match="header"):
+        read_filter(p)
+
+
+def test_rejects_truncated_or_extended_payload(tmp_path, monkeypatch):
+    import torch
+
+    monkeypatch.setattr(torch.cuda, "is_available", lambda: False)
+    raw = open(os.path.join(GOLD, "blowchoc_mix.bwch"), "rb").read()
+    p = tmp_path / "f"
+    p.write_bytes(raw[:-8])
+    with pytest.raises(FilterFormatError):
+        read_filter(p)
+    p.write_bytes(raw + b"\x00")
+    with pytest.raises(FilterFormatError):
+        read_filter(p)
+
+
+def test_toy_width_does_not_serialize():
+    f = bb.Filter.from_config(bb.FilterConfig(kind="blowchoc", k=2, size_bits=64, block_bits=16))
+    with pytest.raises(ValueError):
+        write_filter(f, "/dev/null")
+
+
+def test_u64le_and_text_streams(tmp_path):
+    keys = bb.even_keys(3000, 5)
+    p = tmp_path / "k.u64"
+    keys.astype("<u8").tofile(p)
+    got = np.concatenate(list(read_keys(str(p), "u64le", chunk_size=1000)))
+    np.testing.assert_array_equal(got, keys)
+    p.write_bytes(keys.astype("<u8").tobytes() + b"\x01\x02")
+    with pytest.raises(KeyFormatError, match="truncated"):
+        list(read_keys(str(p), "u64le"))
+    t = tmp_path / "k.txt"
+    t.write_text("\n".join(str(int(v)) for v in keys[:50]) + "\n\n")
+    np.testing.assert_array_equal(np.concatenate(list(read_keys(str(t), "text"))), keys[:50])
+    t.write_text("12\nabc\n")
+    with pytest.raises(KeyFormatError, match="line 2"):
+        list(read_keys(str(t), "text"))
+    t.write_text(str(2**64) + "\n")
+    with pytest.raises(KeyFormatError, match="range"):
+        list(read_keys(str(t), "text"))
+    with pytest.raises(KeyFormatError):
+        list(read_keys(str(t), "nope"))
+    with pytest.raises(KeyFormatError, match="q-gram"):
+        list(read_keys(str(t), "fasta"))
+
+
+@pytest.mark.gpu
+def test_gpu_filter_roundtrip_and_fasta(tmp_path):
+    from oracle import oracle as orc
+
+    cfg = bb.FilterConfig(kind="blowchoc", k=9, n_capacity=50_000, choices=3, seed=4, shards=2)
+    f = bb.Filter.from_config(cfg)
+    keys = bb.even_keys(50_000, 1)
+    f.insert_many(keys)
+    p = tmp_path / "g.bwch"
+    write_filter(f, p)
+    g = read_filter(p)
+    np.testing.assert_array_equal(g.storage.words, f.storage.words)
+    assert g.inserted == f.inserted and g.cost == f.cost
+    probes = np.concatenate([keys[:1000], bb.odd_keys(20_000, 2)])
+    np.testing.assert_array_equal(g.contains_many(probes), f.contains_many(probes))
+    # the reference-written files load onto the device with identical lookups
+    for name in ("blowchoc_mix", "distinct"):
+        h = read_filter(os.path.join(GOLD, name + ".bwch"))
+        pr = np.concatenate([bb.even_keys(index()[name]["n"], 8), bb.odd_keys(3000, 9)])
+        o = orc.make_filter(h.kind, k=h.k, choices=h.choices, strategy=h.strategy,
+                            block_bits=h.block_bits, shards=h.shards, seed=h.seed,
+                            size_bits=h.num_blocks * h.block_bits,
+                            cost_code=h.cost.code, cost_param=h.cost.param)
+        o.words[:] = h.storage.words
+        np.testing.assert_array_equal(h.contains_many(pr), o.contains_many(pr))
+        assert h.contains_many(pr[: index()[name]["n"]]).all()
+    fa = tmp_path / "x.fa"
+    fa.write_bytes(b">r1\nACGTACGTAC\nGTTTACG\n>r2 desc\nNNACGTAAAC\n")
+    chunks = list(read_keys(str(fa), "fasta", q=5))
+    assert len(chunks) == 2
+    np.testing.assert_array_equal(chunks[0], orc.encode_qgrams(b"ACGTACGTACGTTTACG", 5))
+    np.testing.assert_array_equal(chunks[1], orc.encode_qgrams(b"NNACGTAAAC", 5))
