@@ -263,6 +263,47 @@ __device__ __forceinline__ void build_mask_generic(const KParams &p, u64 x, u64 
     }
 }
 
+// Reference insert decision for one key (c >= 2), B = 512 and the random
+// strategy: the mask is built in the thread's private shared-memory column
+// (col = &column[0][lane], stride 32 words) and read back into registers,
+// candidates are read with four L2-coherent LDG.128 each.
+__device__ __forceinline__ void insert_fast512(const KParams &p, u64 *words, u64 x, u32 *col) {
+#pragma unroll
+    for (int w = 0; w < 16; ++w) col[w * 32] = 0u;
+    const u32 xlo = (u32)x, xhi = (u32)(x >> 32);
+#pragma unroll 4
+    for (u32 i = 0; i < p.k; ++i) {
+        const u32 h = bit512(p.bit_a_lo[i], p.bit_a_hi[i], xlo, xhi);
+        col[(h >> 5) * 32] |= 1u << (h & 31);
+    }
+    u32 m[16];
+#pragma unroll
+    for (int w = 0; w < 16; ++w) m[w] = col[w * 32];
+    int best = 0;
+    u32 best_r = 0xffffffffu;
+    for (u32 ci = 0; ci < p.c; ++ci) {
+        const uint4 *src = reinterpret_cast<const uint4 *>(words + block_index(p, x, ci) * 8);
+        u32 j = 0, pr = 0;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const uint4 v = ld_block_cg(src + q);
+            j += __popc(v.x | m[4 * q]) + __popc(v.y | m[4 * q + 1]) +
+                 __popc(v.z | m[4 * q + 2]) + __popc(v.w | m[4 * q + 3]);
+            pr += popc4(v);
+        }
+        const u32 a = j - pr;
+        if (a == 0) return;  // no-op: already represented
+        const u32 r = __ldg(p.rank + j * (p.k + 1) + a);
+        if (r < best_r) {
+            best_r = r;
+            best = (int)ci;
+        }
+    }
+    u64 *dst = words + block_index(p, x, best) * 8;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) red_or(dst + w, (u64)m[2 * w] | ((u64)m[2 * w + 1] << 32));
+}
+
 // Reference insert decision for one key against L2-coherent block reads.
 __device__ __forceinline__ void insert_generic(const KParams &p, u64 *words, u64 x,
                                                const u64 *mask) {

@@ -242,10 +242,12 @@ static int check_device(bc_filter *f) {
 static int ensure_ordered_scratch(bc_filter *f, cudaStream_t s) {
     if (f->d_owner) return BC_OK;
     const u64 M = f->kp.num_blocks;
-    // M/8-key chunks need ~8 claim rounds and ~1.25 visits per key; small
-    // filters are bound by the per-round grid syncs instead, so they take
-    // M/2-key chunks (~12 rounds, ~2 visits per key) -- SURVEY App. B
-    u64 chunk = M < (1ull << 20) ? M / 2 : M / 8;
+    // Chunk size trades claim rounds (grid syncs) against conflicts (visits per
+    // key).  Measured on B200 (bench.py --insert-mode ordered): cfg1 (M = 2^15)
+    // is best at chunk = M (182 Mkeys/s vs 96 at M/8), cfg3 (M = 2^23) at
+    // M/16 = 2^19 (1261 vs 1125 at M/8), i.e. about two keys per resident thread.
+    u64 chunk = std::min<u64>(M, 1ull << 19);
+    if (const char *e = std::getenv("BC_ORDERED_CHUNK")) chunk = std::strtoull(e, nullptr, 10);
     chunk = std::max<u64>(chunk, 256);
     chunk = std::min<u64>(chunk, 1ull << 24);
     CUDA_TRY(cudaMalloc(&f->d_owner, sizeof(u64) * M));

@@ -168,6 +168,9 @@ __global__ void __launch_bounds__(256) ordered_kernel(const __grid_constant__ KP
     cg::grid_group grid = cg::this_grid();
     const u64 gtid = blockIdx.x * (u64)blockDim.x + threadIdx.x;
     const u64 gstride = (u64)gridDim.x * blockDim.x;
+    __shared__ u32 ocol[8][16][32];  // fast path: per-thread mask columns
+    u32 *col = &ocol[threadIdx.x >> 5][0][threadIdx.x & 31];
+    const bool fast = p.fast_random && p.wpb == 8;
     u32 round = __ldcg(state);
     u32 *cur = lists, *nxt = lists + chunk;
     u64 mask[kMaxWpb];
@@ -192,7 +195,9 @@ __global__ void __launch_bounds__(256) ordered_kernel(const __grid_constant__ KP
                 bool win = true;
                 for (u32 ci = 0; ci < p.c; ++ci)
                     win &= __ldcg(owner + block_index(p, x, ci)) == (claim_hi | li);
-                if (win) {
+                if (win && fast) {
+                    insert_fast512(p, words, x, col);
+                } else if (win) {
                     build_mask_generic(p, x, mask);
                     insert_generic(p, words, x, mask);
                 } else {
