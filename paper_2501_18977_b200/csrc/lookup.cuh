@@ -46,17 +46,18 @@ __device__ __forceinline__ bool lookup_tile(const KParams &p, const u64 *__restr
     for (int ci = 0; ci < C; ++ci) {
         if (done == full) break;
         __syncwarp();
-        uint4 w[4];
+        // stage with cp.async (LDGSTS): global -> shared without a register
+        // round trip or a separate STS
 #pragma unroll
         for (int pp = 0; pp < 4; ++pp) {
             const int kk = 4 * g + pp;
-            if (!((done >> kk) & 1u)) w[pp] = ld_block_cg(w4 + (u64)ls.blk[ci][kk] * 4 + s);
+            if (!((done >> kk) & 1u)) {
+                const u32 dst = (u32)__cvta_generic_to_shared(&ls.blocks[stage_row(kk)][s]);
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst),
+                             "l"(w4 + (u64)ls.blk[ci][kk] * 4 + s));
+            }
         }
-#pragma unroll
-        for (int pp = 0; pp < 4; ++pp) {
-            const int kk = 4 * g + pp;
-            if (!((done >> kk) & 1u)) ls.blocks[stage_row(kk)][s] = w[pp];
-        }
+        asm volatile("cp.async.wait_all;" ::: "memory");
         __syncwarp();
         if (!((done >> lane) & 1u)) {
             u32 acc = 1u;
