@@ -13,6 +13,7 @@
 // base most significant; a window touching any other byte is skipped;
 // canonical = min(code, reverse complement).
 #include "blocks.cuh"
+#include "lookup.cuh"
 
 namespace bc {
 
@@ -203,6 +204,37 @@ __global__ void __launch_bounds__(kQgramThreads) qgram_blocks_kernel(
     }
 }
 
+// Lookups with the random strategy: the compacted keys go through the
+// staged-block tile with early exit over the choices (lookup.cuh).
+template <int C>
+__global__ void __launch_bounds__(kQgramThreads) qgram_lookup_kernel(
+    const __grid_constant__ KParams p, const u64 *__restrict__ words, const u8 *__restrict__ seq,
+    u64 len, int q, int canonical, u64 nwin, u64 ntiles, const u64 *__restrict__ tile_off,
+    u8 *__restrict__ out, unsigned long long *__restrict__ hits) {
+    __shared__ QgramSmem qs;
+    __shared__ LookupSmem<C> smem[kWarps];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    LookupSmem<C> &ls = smem[warp];
+    u32 my_hits = 0;
+    for (u64 tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const u32 v = tile_encode(seq, len, q, canonical, tile * kQgramTile, nwin, qs);
+        const u64 obase = tile_off ? tile_off[tile] : 0ull;
+        for (u32 sub = 32u * warp; sub < v; sub += 32u * kWarps) {
+            const bool valid = sub + lane < v;
+            const bool f = lookup_tile<C>(p, words, ls, valid ? qs.keys[sub + lane] : 0ull,
+                                          valid, lane);
+            if (out != nullptr && valid) out[obase + sub + lane] = (u8)f;
+            my_hits += f ? 1u : 0u;
+            __syncwarp();
+        }
+        __syncthreads();
+    }
+    if (hits != nullptr) {
+        for (int o = 16; o > 0; o >>= 1) my_hits += __shfl_xor_sync(kFull, my_hits, o);
+        if (lane == 0 && my_hits) atomicAdd(hits, (unsigned long long)my_hits);
+    }
+}
+
 cudaError_t launch_scan(u64 *v, u64 n, unsigned long long *total, cudaStream_t s) {
     scan_kernel<<<1, 1024, 0, s>>>(v, n, total);
     count_launch();
@@ -246,6 +278,14 @@ static cudaError_t launch_qb(const KParams &p, u64 *words, const u8 *seq, u64 le
     const u64 nwin = n_windows(len, q);
     if (nwin == 0) return cudaSuccess;
     const u64 ntiles = (nwin + kQgramTile - 1) / kQgramTile;
+    if (OP == OP_CONTAINS && p.fast_random && count == nullptr) {
+        const void *fl = (const void *)qgram_lookup_kernel<C>;
+        const unsigned g = grid_for(fl, kQgramThreads, 0, ntiles);
+        qgram_lookup_kernel<C><<<g, kQgramThreads, 0, s>>>(p, words, seq, len, q, canonical,
+                                                           nwin, ntiles, tile_off, out, hits);
+        count_launch();
+        return cudaGetLastError();
+    }
     const void *fn = (const void *)qgram_blocks_kernel<OP, C>;
     const unsigned grid = grid_for(fn, kQgramThreads, 0, ntiles);
     qgram_blocks_kernel<OP, C><<<grid, kQgramThreads, 0, s>>>(p, words, seq, len, q, canonical,
