@@ -416,7 +416,7 @@ def run_ours(args, cfg):
             filt.insert_many(keys)
         ev[1].record(stream)
         if world > 1:
-            dist.broadcast(words, src=0)
+            dist.broadcast(words.view(torch.int64), src=0)
         ev[2].record(stream)
         filt.contains_many(queries, out=out)
         ev[3].record(stream)
@@ -549,7 +549,7 @@ def run_e2e(args, cfg, filt, keys, queries, world, rank, dev):
             words.zero_()
             filt.insert_many(nk)                 # H2D of the keys inside the call
         if world > 1:
-            dist.broadcast(words, src=0)
+            dist.broadcast(words.view(torch.int64), src=0)
         filt.contains_many(nq, out=no)           # H2D queries, D2H answers
 
     steps = max(1, min(args.steps, 5))
@@ -671,7 +671,7 @@ def run_dna(args, cfg):
             res["inserted"] = filt.insert_qgrams(enc, genome)
         ev[1].record(stream)
         if world > 1:
-            dist.broadcast(words, src=0)
+            dist.broadcast(words.view(torch.int64), src=0)
         ev[2].record(stream)
         res["hits_true"] = filt.count_qgram_hits(enc, true_reads)
         res["hits_rand"] = filt.count_qgram_hits(enc, rand_reads)
