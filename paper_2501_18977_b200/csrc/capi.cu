@@ -127,8 +127,17 @@ extern "C" int bc_filter_create(const bc_filter_desc *d, bc_filter **out) {
         return fail(BC_EUNSUP, "block_bits %d above the supported %d", B, kMaxWpb * 64);
     if (d->kind != BC_KIND_STANDARD && d->num_blocks >= (1ull << 32))
         return fail(BC_EUNSUP, "more than 2^32 blocks");
-    for (int i = 0; i < d->k; ++i)
-        if (d->bit_b[i] < 1) return fail(BC_EINVAL, "bit range %d is zero", i);
+    // bit ranges are implied by the layout (BitSelector, hashing.py:118-162):
+    // random -> B for every function, distinct -> B - i, standard -> m = M*B.
+    // Anything else would address bits outside a block.
+    for (int i = 0; i < d->k; ++i) {
+        const u64 want = d->kind == BC_KIND_STANDARD ? d->num_blocks * (u64)B
+                         : d->strategy == 0          ? (u64)B
+                                                     : (u64)(B - i);
+        if (d->bit_b[i] != want)
+            return fail(BC_EINVAL, "bit range %d is %llu, expected %llu", i,
+                        (unsigned long long)d->bit_b[i], (unsigned long long)want);
+    }
 
     bc_filter *f = new (std::nothrow) bc_filter();
     if (!f) return fail(BC_ENOMEM, "out of host memory");
@@ -588,6 +597,10 @@ static int host_pipeline(bc_filter *f, u64 *words, const u64 *h_keys, u64 n, int
     // the copy streams must not start before earlier work on `s`
     cudaEvent_t start;
     CUDA_TRY(cudaEventCreateWithFlags(&start, cudaEventDisableTiming));
+    struct EventGuard {
+        cudaEvent_t e;
+        ~EventGuard() { cudaEventDestroy(e); }
+    } start_guard{start};
     CUDA_TRY(cudaEventRecord(start, s));
     for (int b = 0; b < 2; ++b) CUDA_TRY(cudaStreamWaitEvent(st->cs[b], start, 0));
 
@@ -641,7 +654,6 @@ static int host_pipeline(bc_filter *f, u64 *words, const u64 *h_keys, u64 n, int
         *h_hits += v;
     }
     CUDA_TRY(cudaStreamSynchronize(s));
-    cudaEventDestroy(start);
     return rc;
 }
 

@@ -193,6 +193,12 @@ def test_abi_argument_errors_without_gpu():
     h = ctypes.c_void_p()
     assert L.bc_filter_create(ctypes.byref(d), ctypes.byref(h)) == _native.BC_EINVAL
     assert b"choices" in L.bc_last_error()
+    # bit ranges must match the layout: random -> B (here 3 != 512)
+    d.choices = 2
+    assert L.bc_filter_create(ctypes.byref(d), ctypes.byref(h)) == _native.BC_EINVAL
+    assert b"bit range 0" in L.bc_last_error()
+    d.kind, d.choices, d.block_bits = 1, 1, 8
+    assert L.bc_filter_create(ctypes.byref(d), ctypes.byref(h)) == _native.BC_EINVAL
 
 
 def test_partition_by_shard_is_stable():
