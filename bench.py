@@ -84,6 +84,10 @@ def parse():
 
 # -- distributed plumbing ---------------------------------------------------------------
 
+# launched by torchrun (even with one rank): use torch.distributed / NCCL
+DIST = "RANK" in os.environ and "LOCAL_RANK" in os.environ
+
+
 def dist_env():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -393,7 +397,7 @@ def run_ours(args, cfg):
     from paper_2501_18977_b200 import _native
 
     world, rank, local = dist_env()
-    if world > 1:
+    if DIST:
         torch.cuda.set_device(local)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     else:
@@ -415,7 +419,7 @@ def run_ours(args, cfg):
             words.zero_()
             filt.insert_many(keys)
         ev[1].record(stream)
-        if world > 1:
+        if DIST:
             dist.broadcast(words.view(torch.int64), src=0)
         ev[2].record(stream)
         filt.contains_many(queries, out=out)
@@ -428,7 +432,7 @@ def run_ours(args, cfg):
     for i in range(args.warmup):
         step(events[i])
     torch.cuda.synchronize()
-    if world > 1:
+    if DIST:
         dist.barrier()
     torch.cuda.synchronize()
     l0 = _native.launch_count()
@@ -440,7 +444,7 @@ def run_ours(args, cfg):
     t1.record(stream)
     torch.cuda.synchronize()
     launches = _native.launch_count() - l0
-    if world > 1:
+    if DIST:
         dist.barrier()
     torch.cuda.synchronize()
     clocks = sampler.stop()
@@ -449,7 +453,7 @@ def run_ours(args, cfg):
     ins_ms = sum(e[0].elapsed_time(e[1]) for e in timed) / args.steps
     bc_ms = sum(e[1].elapsed_time(e[2]) for e in timed) / args.steps
     look_ms = sum(e[2].elapsed_time(e[3]) for e in timed) / args.steps
-    if world > 1:
+    if DIST:
         t = torch.tensor([elapsed_ms], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         elapsed_ms = float(t.item())
@@ -462,7 +466,7 @@ def run_ours(args, cfg):
     fn = int((is_pos & ~found).sum().item())
     n_neg = int((~is_pos).sum().item())
     fp = int((~is_pos & found).sum().item())
-    if world > 1:
+    if DIST:
         t = torch.tensor([fn, fp, n_neg], device=dev, dtype=torch.int64)
         dist.all_reduce(t)
         fn, fp, n_neg = (int(v) for v in t.tolist())
@@ -508,7 +512,7 @@ def run_ours(args, cfg):
                    "l2": "inputs larger than L2 (keys re-read every step)"},
         "insert_mkeys_s": round(cfg["n"] / ins_ms / 1e3, 2) if builder else None,
         "lookup_mkeys_s": round(cfg["nq"] / look_ms / 1e3, 2),
-        "broadcast_ms": round(bc_ms, 3) if world > 1 else None,
+        "broadcast_ms": round(bc_ms, 3) if DIST else None,
         "false_negatives": fn, "fpr": fp / max(n_neg, 1),
         "gpu_launches": int(launches),
         "clocks": clocks,
@@ -524,7 +528,7 @@ def run_ours(args, cfg):
         line["cpu_baseline"] = cpu_rate(cfg, filt.storage.words)
     if rank == 0:
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if DIST:
         dist.barrier()
         dist.destroy_process_group()
 
@@ -548,7 +552,7 @@ def run_e2e(args, cfg, filt, keys, queries, world, rank, dev):
         if builder:
             words.zero_()
             filt.insert_many(nk)                 # H2D of the keys inside the call
-        if world > 1:
+        if DIST:
             dist.broadcast(words.view(torch.int64), src=0)
         filt.contains_many(nq, out=no)           # H2D queries, D2H answers
 
@@ -556,14 +560,14 @@ def run_e2e(args, cfg, filt, keys, queries, world, rank, dev):
     for _ in range(max(1, min(args.warmup, 2))):
         step()
     torch.cuda.synchronize()
-    if world > 1:
+    if DIST:
         dist.barrier()
     t0 = time.perf_counter()
     for _ in range(steps):
         step()
     torch.cuda.synchronize()
     el = time.perf_counter() - t0
-    if world > 1:
+    if DIST:
         t = torch.tensor([el], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         el = float(t.item())
@@ -643,7 +647,7 @@ def run_dna(args, cfg):
     from paper_2501_18977_b200 import _native
 
     world, rank, local = dist_env()
-    if world > 1:
+    if DIST:
         torch.cuda.set_device(local)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     else:
@@ -670,7 +674,7 @@ def run_dna(args, cfg):
             words.zero_()
             res["inserted"] = filt.insert_qgrams(enc, genome)
         ev[1].record(stream)
-        if world > 1:
+        if DIST:
             dist.broadcast(words.view(torch.int64), src=0)
         ev[2].record(stream)
         res["hits_true"] = filt.count_qgram_hits(enc, true_reads)
@@ -684,7 +688,7 @@ def run_dna(args, cfg):
     for i in range(args.warmup):
         step(events[i])
     torch.cuda.synchronize()
-    if world > 1:
+    if DIST:
         dist.barrier()
     l0 = _native.launch_count()
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -696,7 +700,7 @@ def run_dna(args, cfg):
     launches = _native.launch_count() - l0
     clocks = sampler.stop()
     elapsed = t0.elapsed_time(t1)
-    if world > 1:
+    if DIST:
         t = torch.tensor([elapsed], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         elapsed = float(t.item())
@@ -740,7 +744,7 @@ def run_dna(args, cfg):
         line["cpu_baseline"] = cpu_dna_rate(cfg)
     if rank == 0:
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if DIST:
         dist.destroy_process_group()
 
 

@@ -121,3 +121,45 @@ def test_slice_bounds_cover():
             assert b[0][0] == 0 and b[-1][1] == n
             assert all(b[i][1] == b[i + 1][0] for i in range(w - 1))
             assert max(h - l for l, h in b) - min(h - l for l, h in b) <= 1
+
+
+def _nccl_worker(rank, world, port):
+    import torch
+
+    import paper_2501_18977_b200 as bb
+    from paper_2501_18977_b200 import distributed as D
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(rank)
+    dist.init_process_group("nccl", rank=rank, world_size=world,
+                            device_id=torch.device("cuda", rank))
+    try:
+        cfg = bb.FilterConfig(kind="blowchoc", k=7, choices=2, n_capacity=20_000, shards=4,
+                              seed=17)
+        keys = bb.even_keys(20_000, 5)
+        f = bb.Filter.from_config(cfg)
+        mine = D.owned_keys(f, torch.from_numpy(keys).cuda(), rank, world)
+        f.insert_many(mine)
+        D.gather_subfilters(f)
+        ref = orc.make_filter(**CFG)
+        ref.insert_many(keys)
+        assert np.array_equal(f.storage.words, ref.words)
+        D.broadcast_filter(f, src=0)
+        probes = np.concatenate([keys[:5000], orc.odd_keys(7001, 9)])
+        assert np.array_equal(D.contains_many_sharded(f, probes), ref.contains_many(probes))
+        assert D.count_hits_sharded(f, probes) == int(ref.contains_many(probes).sum())
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_nccl_collectives_on_device():
+    """The NCCL code paths (all_gather_into_tensor of subfilter ranges,
+    broadcast, key-sharded lookups) on the GPUs present (world = #GPUs)."""
+    import torch
+
+    world = torch.cuda.device_count()
+    if 4 % world:  # the test filter has 4 shards
+        world = 1
+    mp.spawn(_nccl_worker, args=(world, free_port()), nprocs=world, join=True)
