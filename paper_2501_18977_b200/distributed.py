@@ -114,8 +114,11 @@ def owned_keys(filt, keys, rank: int, world: int):
     per = filt.shards // world
     shard = filt.route_many(keys)
     if isinstance(shard, torch.Tensor):
+        # torch has no compare / index kernels for uint64: work on int64 views
+        shard = shard.view(torch.int64)  # shard ids < T, no sign issue
         sel = (shard >= rank * per) & (shard < (rank + 1) * per)
-        return keys[sel]
+        k64 = keys.view(torch.int64) if keys.dtype == torch.uint64 else keys
+        return k64[sel]
     shard = np.asarray(shard)
     sel = (shard >= rank * per) & (shard < (rank + 1) * per)
     return np.asarray(keys)[sel]
