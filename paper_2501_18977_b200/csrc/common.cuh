@@ -117,7 +117,16 @@ __device__ __forceinline__ uint4 ld_block_nc(const uint4 *p) {
 }
 
 // L2-coherent gather (inserts: other CTAs are OR-ing into the same array).
-__device__ __forceinline__ uint4 ld_block_cg(const uint4 *p) { return __ldcg(p); }
+// The .L2::64B size hint keeps an L2 miss on a random block from being filled
+// as a whole 128-byte line: without it the DRAM reads of a random 64-byte
+// gather are 2x the data (tools/gather_probe.cu + ncu, profiles/r1).
+__device__ __forceinline__ uint4 ld_block_cg(const uint4 *p) {
+    uint4 r;
+    asm volatile("ld.global.cg.L2::64B.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                 : "l"(p));
+    return r;
+}
 
 __device__ __forceinline__ void red_or(u64 *p, u64 v) {
     if (v) atomicOr((unsigned long long *)p, (unsigned long long)v);

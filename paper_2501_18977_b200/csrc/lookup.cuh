@@ -53,7 +53,7 @@ __device__ __forceinline__ bool lookup_tile(const KParams &p, const u64 *__restr
             const int kk = 4 * g + pp;
             if (!((done >> kk) & 1u)) {
                 const u32 dst = (u32)__cvta_generic_to_shared(&ls.blocks[stage_row(kk)][s]);
-                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst),
+                asm volatile("cp.async.cg.shared.global.L2::64B [%0], [%1], 16;" ::"r"(dst),
                              "l"(w4 + (u64)ls.blk[ci][kk] * 4 + s));
             }
         }

@@ -101,6 +101,34 @@ extern "C" int scatter_main(u64 mib, int lg);
 
 int main(int argc, char **argv) {
     if (argc > 1 && argv[1][0] == 's') return scatter_main(strtoull(argv[2], 0, 10), atoi(argv[3]));
+    if (argc > 5 && argv[1][0] == 'g') {
+        // single variant: g <MiB> <lookups log2> <variant 0..4> <L2 fetch granularity 0|32|64|128>
+        const u64 mib = strtoull(argv[2], 0, 10), n = 1ull << atoi(argv[3]);
+        const int v = atoi(argv[4]);
+        const size_t gran = strtoull(argv[5], 0, 10);
+        const u64 nb = mib * (1ull << 20) / 64;
+        uint4 *blocks;
+        u64 *keys;
+        unsigned char *out;
+        cudaMalloc(&blocks, nb * 64);
+        cudaMalloc(&keys, n * 8);
+        cudaMalloc(&out, n);
+        fill<<<1184, 256>>>((u64 *)blocks, nb * 8);
+        fill<<<1184, 256>>>(keys, n);
+        if (gran) cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, gran);
+        float ms = 0;
+        switch (v) {
+            case 0: ms = run<0, 2>(blocks, nb, keys, n, out, 1); break;
+            case 1: ms = run<1, 2>(blocks, nb, keys, n, out, 1); break;
+            case 2: ms = run<2, 2>(blocks, nb, keys, n, out, 1); break;
+            case 3: ms = run<3, 2>(blocks, nb, keys, n, out, 1); break;
+            default: ms = run<4, 2>(blocks, nb, keys, n, out, 1); break;
+        }
+        size_t g = 0;
+        cudaDeviceGetLimit(&g, cudaLimitMaxL2FetchGranularity);
+        printf("variant %d gran %zu: %.3f ms, %.1f G lookups/s\n", v, g, ms, n / ms / 1e6);
+        return 0;
+    }
     const u64 mib = argc > 1 ? strtoull(argv[1], 0, 10) : 512;
     const int lg = argc > 2 ? atoi(argv[2]) : 27;
     const int only = argc > 3 ? atoi(argv[3]) : -1;
