@@ -134,22 +134,22 @@ def make_inputs(cfg: dict, rank: int, device):
         is_pos = perm < npos
         return (torch.from_numpy(keys).to(device), torch.from_numpy(q).to(device),
                 torch.from_numpy(is_pos).to(device))
+    from paper_2501_18977_b200 import even_keys, odd_keys
+
+    # the reference's own streams (even_keys(n, 11) / odd_keys(., 12)),
+    # generated on the device bit-identically to numpy (bc_pcg64_fill)
     g = torch.Generator(device=device).manual_seed(1234 + rank)
-    span = 1 << 28  # generate in slices: cfg5 holds 5e9 keys + 4e9 queries (~80 GB)
-    keys = torch.empty(n, dtype=torch.int64, device=device)
-    for a in range(0, n, span):
-        b = min(n, a + span)
-        keys[a:b] = torch.randint(-2**63, 2**63 - 1, (b - a,), device=device,
-                                  dtype=torch.int64, generator=g) & ~1
-    # queries: half uniform samples of the inserted keys, half odd (never inserted)
+    span = 1 << 28  # slices: cfg5 holds 5e9 keys + 4e9 queries (~80 GB)
+    keys = even_keys(n, 11, device=device).view(torch.int64)
+    # queries: a seeded coin picks a uniform sample of the inserted keys
+    # (positive) or the next key of the odd stream (negative)
     q = torch.empty(nq, dtype=torch.int64, device=device)
     sel = torch.empty(nq, dtype=torch.bool, device=device)
     for a in range(0, nq, span):
         b = min(nq, a + span)
         s = torch.randint(0, 2, (b - a,), device=device, dtype=torch.int64, generator=g).bool()
         idx = torch.randint(0, n, (b - a,), device=device, dtype=torch.int64, generator=g)
-        neg = torch.randint(-2**63, 2**63 - 1, (b - a,), device=device, dtype=torch.int64,
-                            generator=g) | 1
+        neg = odd_keys(b - a, 12 + rank, device=device, offset=a).view(torch.int64)
         q[a:b] = torch.where(s, keys[idx], neg)
         sel[a:b] = s
         del s, idx, neg
@@ -506,7 +506,9 @@ def run_ours(args, cfg):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64",
         "data": ("synthetic: reference key streams even_keys/odd_keys, seeded shuffle"
-                 if cfg["ref_keys"] else "synthetic: seeded device-generated uint64 keys"),
+                 if cfg["ref_keys"] else
+                 "synthetic: reference key streams even_keys(n, 11) / odd_keys(., 12) "
+                 "generated on the device (bit-identical to numpy), seeded 50/50 mix"),
         "config": {"workload": cfg["workload"], "insert_mode": mode,
                    "parallelism": f"build on rank 0 + NCCL broadcast, lookups dp{world}",
                    "l2": "inputs larger than L2 (keys re-read every step)"},

@@ -155,6 +155,15 @@ BC_API int bc_route(bc_filter *f, const uint64_t *d_keys, uint64_t n, uint64_t *
 BC_API int bc_eval_hash(uint64_t a, uint64_t b, const uint64_t *d_keys, uint64_t n,
                  uint64_t *d_out, void *stream);
 
+/* The reference's key streams on the device: outputs [offset, offset+n) of
+ * numpy's default_rng(seed).integers(0, 2**64, dtype=uint64) -- PCG64 from
+ * the seeded 128-bit (state, inc) that numpy reports -- each masked as
+ * (v & and_mask) | or_mask.  even_keys: and_mask = ~1; odd_keys: or_mask = 1
+ * (analysis.py:34-43). */
+BC_API int bc_pcg64_fill(uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi, uint64_t inc_lo,
+                         uint64_t offset, uint64_t n, uint64_t and_mask, uint64_t or_mask,
+                         uint64_t *d_out, void *stream);
+
 /* Thread-local description of the last error on this thread. */
 BC_API const char *bc_last_error(void);
 

@@ -23,7 +23,7 @@ EXPORTS = (
     "bc_filter_create", "bc_filter_destroy", "bc_insert", "bc_contains",
     "bc_insert_host", "bc_contains_host", "bc_encode_qgrams", "bc_insert_qgrams",
     "bc_contains_qgrams", "bc_block_histogram", "bc_route", "bc_eval_hash",
-    "bc_last_error", "bc_launch_count", "bc_version",
+    "bc_last_error", "bc_launch_count", "bc_version", "bc_pcg64_fill",
 )
 
 
@@ -84,6 +84,7 @@ def lib() -> ctypes.CDLL:
         L.bc_block_histogram.argtypes = [P, u64, ci, P, P]
         L.bc_route.argtypes = [P, P, u64, P, P]
         L.bc_eval_hash.argtypes = [u64, u64, P, u64, P, P]
+        L.bc_pcg64_fill.argtypes = [u64, u64, u64, u64, u64, u64, u64, u64, P, P]
         L.bc_last_error.restype = ctypes.c_char_p
         L.bc_launch_count.restype = ctypes.c_ulonglong
         L.bc_version.restype = ctypes.c_char_p
@@ -92,7 +93,8 @@ def lib() -> ctypes.CDLL:
             if fn.restype is ctypes.c_int or name in (
                     "bc_filter_create", "bc_insert", "bc_contains", "bc_insert_host",
                     "bc_contains_host", "bc_encode_qgrams", "bc_insert_qgrams",
-                    "bc_contains_qgrams", "bc_block_histogram", "bc_route", "bc_eval_hash"):
+                    "bc_contains_qgrams", "bc_block_histogram", "bc_route", "bc_eval_hash",
+                    "bc_pcg64_fill"):
                 fn.restype = ctypes.c_int
         _lib = L
         return L

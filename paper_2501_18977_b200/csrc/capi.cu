@@ -523,6 +523,16 @@ extern "C" int bc_eval_hash(uint64_t a, uint64_t b, const uint64_t *d_keys, uint
     return BC_OK;
 }
 
+extern "C" int bc_pcg64_fill(uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi,
+                             uint64_t inc_lo, uint64_t offset, uint64_t n, uint64_t and_mask,
+                             uint64_t or_mask, uint64_t *d_out, void *stream) {
+    if (n && !d_out) return fail(BC_EINVAL, "null output");
+    if (!(inc_lo & 1)) return fail(BC_EINVAL, "PCG64 increment must be odd");
+    CUDA_TRY(launch_pcg64_fill(state_hi, state_lo, inc_hi, inc_lo, offset, n, and_mask, or_mask,
+                               d_out, (cudaStream_t)stream));
+    return BC_OK;
+}
+
 // ---- host-buffer entry points ---------------------------------------------------------
 // Per-device staging: two pinned key buffers, two pinned answer buffers, two
 // device key/answer buffers and two copy streams, so the copy of chunk i+1

@@ -50,6 +50,11 @@ cudaError_t launch_qgram_blocks(int op, const KParams &p, u64 *words, const u8 *
                                 unsigned long long *hits, unsigned long long *count,
                                 cudaStream_t s);
 
+// numpy PCG64 stream (default_rng(seed).integers(0, 2**64, uint64)) from a
+// seeded (state, inc): outputs [offset, offset+n), then & and_mask | or_mask.
+cudaError_t launch_pcg64_fill(u64 state_hi, u64 state_lo, u64 inc_hi, u64 inc_lo, u64 offset,
+                              u64 n, u64 and_mask, u64 or_mask, u64 *out, cudaStream_t s);
+
 // In-place exclusive scan of n u64 by one CTA (*total = sum, nullable).
 cudaError_t launch_scan(u64 *v, u64 n, unsigned long long *total, cudaStream_t s);
 

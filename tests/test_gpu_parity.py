@@ -341,6 +341,31 @@ def test_fused_qgram_insert_single_choice_and_relaxed():
     assert g.count_qgram_hits(enc, genome) == keys.shape[0]
 
 
+@pytest.mark.parametrize("seed", [0, 11, 12, 5, 2**40 + 7])
+def test_device_key_streams_equal_numpy(seed):
+    """even_keys / odd_keys generated on the GPU (PCG64 jump-ahead) are
+    bit-identical to the reference's numpy streams, at any offset."""
+    for n in (1, 63, 64, 65, 4097, 100_003):
+        np.testing.assert_array_equal(bb.even_keys(n, seed, device="cuda").cpu().numpy(),
+                                      bb.even_keys(n, seed))
+        np.testing.assert_array_equal(bb.odd_keys(n, seed, device="cuda").cpu().numpy(),
+                                      bb.odd_keys(n, seed))
+    full = bb.even_keys(300_000, seed)
+    for off in (1, 77, 4096, 123_456):
+        got = bb.even_keys(1000, seed, device="cuda", offset=off).cpu().numpy()
+        np.testing.assert_array_equal(got, full[off:off + 1000])
+
+
+def test_estimate_fpr_device_stream_matches_host():
+    cfg = bb.FilterConfig(kind="blowchoc", k=8, n_capacity=100_000, choices=2, seed=3)
+    f = bb.Filter.from_config(cfg)
+    f.insert_many(bb.even_keys(100_000, 4))
+    est = bb.estimate_fpr(f, n_queries=3 * 2**18 + 5, chunk_size=2**18, seed=99)
+    host = sum(f.count_hits(bb.odd_keys(min(2**18, 3 * 2**18 + 5 - a), bb.derive_seed(99, i)))
+               for i, a in enumerate(range(0, 3 * 2**18 + 5, 2**18)))
+    assert est.false_positives == host
+
+
 def test_partitioned_single_choice_insert_bit_identical(golden, tmp_path):
     """The opt-in region-partitioned insert (BC_PARTITION_MIN_KEYS) gives the
     reference's bit array (run in a subprocess: the knob is read at load)."""
