@@ -71,12 +71,16 @@ __global__ void __launch_bounds__(kTPB) blocks512_kernel(const __grid_constant__
     const u64 ntiles = (n + 31) / 32;
     const u64 nwarps = (u64)gridDim.x * kWarps;
     u32 my_hits = 0;
-    for (u64 tile = blockIdx.x * (u64)kWarps + (threadIdx.x >> 5); tile < ntiles;
-         tile += nwarps) {
+    u64 tile = blockIdx.x * (u64)kWarps + (threadIdx.x >> 5);
+    // the next tile's key is loaded while the current tile is processed
+    u64 x_next = tile * 32 + lane < n ? ld_stream(keys + tile * 32 + lane) : 0ull;
+    for (; tile < ntiles; tile += nwarps) {
         const u64 base = tile * 32;
         const u32 cnt = (u32)min((u64)32, n - base);
         const bool valid = (u32)lane < cnt;
-        const u64 x = valid ? ld_stream(keys + base + lane) : 0ull;
+        const u64 x = x_next;
+        const u64 nb = base + nwarps * 32 + lane;
+        x_next = nb < n ? ld_stream(keys + nb) : 0ull;
         phase1<C>(p, x, valid, ws, lane);
         __syncwarp();
         const u32 found = phase2<OP, C>(p, words, ws, lane);
@@ -103,11 +107,15 @@ __global__ void __launch_bounds__(kTPB) lookup512_kernel(const __grid_constant__
     const u64 ntiles = (n + 31) / 32;
     const u64 nwarps = (u64)gridDim.x * kWarps;
     u32 my_hits = 0;
-    for (u64 tile = blockIdx.x * (u64)kWarps + (threadIdx.x >> 5); tile < ntiles;
-         tile += nwarps) {
+    u64 tile = blockIdx.x * (u64)kWarps + (threadIdx.x >> 5);
+    // the next tile's key is loaded while the current tile is probed
+    u64 x_next = tile * 32 + lane < n ? ld_stream(keys + tile * 32 + lane) : 0ull;
+    for (; tile < ntiles; tile += nwarps) {
         const u64 base = tile * 32;
         const bool valid = base + lane < n;
-        const u64 x = valid ? ld_stream(keys + base + lane) : 0ull;
+        const u64 x = x_next;
+        const u64 nb = base + nwarps * 32 + lane;
+        x_next = nb < n ? ld_stream(keys + nb) : 0ull;
         const bool f = lookup_tile<C>(p, words, ls, x, valid, lane);
         if (out != nullptr && valid) out[base + lane] = (u8)f;
         my_hits += f ? 1u : 0u;
