@@ -278,20 +278,6 @@ static const u64 kPartitionMinKeys = []() -> u64 {
     return e ? std::strtoull(e, nullptr, 10) : ~0ull;
 }();
 
-// Opt-in (BC_REGION_SORT=1): relaxed multi-choice inserts bucket each batch by
-// the 2^shift-block region of the first candidate (region_sort.cu).  Measured
-// on B200: cfg5 inserts +13% (FPR +2%), cfg3 -16% with FPR +23% (the keys in
-// flight crowd one region), so it is off by default.  BC_REGION_SORT_SHIFT
-// sets the region size (default 2^19 blocks = 32 MiB).
-static const bool kRegionSortOn = []() {
-    const char *e = std::getenv("BC_REGION_SORT");
-    return e && e[0] == '1';
-}();
-static const u32 kRegionSortShift = []() -> u32 {
-    const char *e = std::getenv("BC_REGION_SORT_SHIFT");
-    return e ? (u32)std::strtoul(e, nullptr, 10) : 19u;
-}();
-
 static int insert_device(bc_filter *f, u64 *words, const u64 *keys, u64 n, int mode,
                          cudaStream_t s) {
     if (n == 0) return BC_OK;
@@ -324,25 +310,6 @@ static int insert_device(bc_filter *f, u64 *words, const u64 *keys, u64 n, int m
         if (per >= 256) {
             KParams kp = f->kp;
             kp.max_ctas = (u32)std::min<u64>(per / 256, 0xffffffffu);
-            const u32 nb = region_sort_buckets(kp, kRegionSortShift);
-            if (kRegionSortOn && kp.wpb == 8 && nb >= 4 && nb <= 1024 && n >= (1ull << 22)) {
-                // region-ordered (region_sort.cu): first-candidate traffic from L2
-                const u64 chunk = std::min<u64>(n, 1ull << 30);
-                u64 *sorted = nullptr;
-                unsigned long long *ctr = nullptr;
-                CUDA_TRY(cudaMallocAsync((void **)&sorted, sizeof(u64) * chunk, s));
-                cudaError_t e = cudaMallocAsync((void **)&ctr, sizeof(u64) * 2 * nb, s);
-                for (u64 off = 0; off < n && e == cudaSuccess; off += chunk) {
-                    const u64 len = std::min(chunk, n - off);
-                    e = launch_region_sort(kp, keys + off, len, kRegionSortShift, sorted, ctr, s);
-                    if (e == cudaSuccess)
-                        e = launch_blocks(OP_INSERT, kp, words, sorted, len, nullptr, nullptr, s);
-                }
-                cudaFreeAsync(ctr, s);
-                cudaFreeAsync(sorted, s);
-                CUDA_TRY(e);
-                return BC_OK;
-            }
             CUDA_TRY(launch_blocks(OP_INSERT, kp, words, keys, n, nullptr, nullptr, s));
             return BC_OK;
         }

@@ -55,13 +55,6 @@ cudaError_t launch_qgram_blocks(int op, const KParams &p, u64 *words, const u8 *
 cudaError_t launch_pcg64_fill(u64 state_hi, u64 state_lo, u64 inc_hi, u64 inc_lo, u64 offset,
                               u64 n, u64 and_mask, u64 or_mask, u64 *out, cudaStream_t s);
 
-// ---- region-ordered relaxed inserts (region_sort.cu) -------------------------------
-// Buckets keys by region (2^shift blocks) of their first candidate: out[] holds
-// the n keys grouped by region; scratch holds 2 * buckets u64 counters.
-u32 region_sort_buckets(const KParams &p, u32 shift);
-cudaError_t launch_region_sort(const KParams &p, const u64 *keys, u64 n, u32 shift, u64 *out,
-                               unsigned long long *scratch, cudaStream_t s);
-
 // In-place exclusive scan of n u64 by one CTA (*total = sum, nullable).
 cudaError_t launch_scan(u64 *v, u64 n, unsigned long long *total, cudaStream_t s);
 

@@ -385,3 +385,4 @@ def test_partitioned_single_choice_insert_bit_identical(golden, tmp_path):
                          cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
     assert out.returncode == 0, out.stderr
     assert out.stdout.strip().splitlines()[-1] == case["words_sha256"]
+
