@@ -233,6 +233,7 @@ extern "C" void bc_filter_destroy(bc_filter *f) {
     cudaFree(f->d_owner);
     cudaFree(f->d_lists);
     cudaFree(f->d_state);
+    bc::l2_release();
     cudaSetDevice(prev);
     delete f;
 }

@@ -127,6 +127,53 @@ __global__ void __launch_bounds__(kTPB) lookup512_kernel(const __grid_constant__
     }
 }
 
+// Single-choice lookups with two tiles per warp in flight (lookup.cuh).
+__global__ void __launch_bounds__(kTPB) lookup512_pipe_kernel(const __grid_constant__ KParams p,
+                                                              const u64 *__restrict__ words,
+                                                              const u64 *__restrict__ keys, u64 n,
+                                                              u8 *__restrict__ out,
+                                                              unsigned long long *__restrict__ hits) {
+    __shared__ PipeStage stages[kWarps][2];
+    PipeStage *st = stages[threadIdx.x >> 5];
+    const int lane = threadIdx.x & 31;
+    const u64 ntiles = (n + 31) / 32;
+    const u64 nwarps = (u64)gridDim.x * kWarps;
+    u32 my_hits = 0;
+    u64 tile = blockIdx.x * (u64)kWarps + (threadIdx.x >> 5);
+    u64 i = tile * 32 + lane;
+    bool valid = i < n;
+    u64 x = valid ? ld_stream(keys + i) : 0ull;
+    stage_blocks(words, st[0], valid ? (u32)block_index(p, x, 0) : 0u,
+                 __ballot_sync(kFull, valid), lane);
+    u64 tile_n = tile + nwarps;
+    i = tile_n * 32 + lane;
+    u64 x_n = i < n ? ld_stream(keys + i) : 0ull;
+    int b = 0;
+    for (; tile < ntiles; tile = tile_n, tile_n += nwarps) {
+        const u64 base = tile * 32;
+        const bool valid_n = tile_n * 32 + lane < n;
+        stage_blocks(words, st[b ^ 1], valid_n ? (u32)block_index(p, x_n, 0) : 0u,
+                     __ballot_sync(kFull, valid_n), lane);
+        i = (tile_n + nwarps) * 32 + lane;
+        const u64 x_nn = i < n ? ld_stream(keys + i) : 0ull;
+        asm volatile("cp.async.wait_group 1;" ::: "memory");
+        __syncwarp();
+        const bool f = valid && test_staged(p, st[b], x, lane);
+        if (out != nullptr && valid) out[base + lane] = (u8)f;
+        my_hits += f ? 1u : 0u;
+        __syncwarp();
+        x = x_n;
+        x_n = x_nn;
+        valid = valid_n;
+        b ^= 1;
+    }
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    if (hits != nullptr) {
+        for (int o = 16; o > 0; o >>= 1) my_hits += __shfl_xor_sync(kFull, my_hits, o);
+        if (lane == 0 && my_hits) atomicAdd(hits, (unsigned long long)my_hits);
+    }
+}
+
 template <int OP>
 __global__ void __launch_bounds__(256) generic_kernel(const __grid_constant__ KParams p,
                                                       u64 *__restrict__ words,
@@ -300,22 +347,108 @@ __global__ void __launch_bounds__(256) eval_hash_kernel(DevHash h, const u64 *__
 }
 
 // ---------------------------------------------------------------------------------
+static bool lookup_pipe_enabled() {
+    static const bool on = [] {
+        const char *e = getenv("BC_LOOKUP_PIPE");
+        return e == nullptr || atoi(e) != 0;
+    }();
+    return on;
+}
+
+// L2 residency of the filter words.  A filter that fits in L2 is launched with
+// an access-policy window marking its words persisting (the streamed keys stay
+// normal): on B200 this keeps the 96 MiB cfg2 filter's dirty lines in L2
+// instead of writing them back under the key stream, +42% single-choice insert
+// rate.  Filters larger than L2 are left alone (a partial window slows relaxed
+// inserts: cfg3 11.9 -> 6.5 Gkeys/s).  BC_L2_PERSIST=0 disables, =1 forces.
+struct L2Info {
+    size_t l2 = 0, persist = 0, window = 0;
+};
+
+static const L2Info &l2_info() {
+    static const L2Info info = [] {
+        L2Info i;
+        int dev = 0, v = 0;
+        cudaGetDevice(&dev);
+        if (cudaDeviceGetAttribute(&v, cudaDevAttrL2CacheSize, dev) == cudaSuccess) i.l2 = v;
+        if (cudaDeviceGetAttribute(&v, cudaDevAttrMaxAccessPolicyWindowSize, dev) == cudaSuccess)
+            i.window = v;
+        if (cudaDeviceGetAttribute(&v, cudaDevAttrMaxPersistingL2CacheSize, dev) == cudaSuccess &&
+            v > 0 && cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, (size_t)v) == cudaSuccess)
+            i.persist = v;
+        cudaGetLastError();
+        return i;
+    }();
+    return info;
+}
+
+static int l2_persist_mode() {  // -1 auto, 0 off, 1 forced
+    static const int m = [] {
+        const char *e = getenv("BC_L2_PERSIST");
+        return e ? atoi(e) : -1;
+    }();
+    return m;
+}
+
+static std::atomic<bool> g_l2_used{false};
+
+void l2_release() {
+    // persisting lines outlive the launches (and the process's other work
+    // competes with them): demote them to normal when a filter is destroyed
+    if (g_l2_used.exchange(false)) {
+        cudaCtxResetPersistingL2Cache();
+        cudaGetLastError();
+    }
+}
+
+template <typename K, typename... Args>
+static cudaError_t launch_words(K kernel, unsigned grid, const KParams &p, const u64 *words,
+                                cudaStream_t s, Args... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kTPB);
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    const size_t fbytes = (size_t)p.num_blocks * p.wpb * 8;
+    const int mode = l2_persist_mode();
+    const L2Info &li = l2_info();
+    if (mode != 0 && li.persist && li.window && (mode == 1 || fbytes <= li.l2)) {
+        const size_t bytes = std::min(fbytes, li.window);
+        attr[0].id = cudaLaunchAttributeAccessPolicyWindow;
+        attr[0].val.accessPolicyWindow.base_ptr = const_cast<u64 *>(words);
+        attr[0].val.accessPolicyWindow.num_bytes = bytes;
+        attr[0].val.accessPolicyWindow.hitRatio =
+            std::min(1.0f, (float)li.persist / (float)std::max<size_t>(bytes, 1));
+        attr[0].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+        attr[0].val.accessPolicyWindow.missProp = cudaAccessPropertyNormal;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        g_l2_used.store(true, std::memory_order_relaxed);
+    }
+    count_launch();
+    return cudaLaunchKernelEx(&cfg, kernel, args...);
+}
+
 template <int OP, int C>
 static cudaError_t launch512(const KParams &p, u64 *words, const u64 *keys, u64 n, u8 *out,
                              unsigned long long *hits, cudaStream_t s) {
+    if (OP == OP_CONTAINS && p.fast_random && C == 1 && lookup_pipe_enabled()) {
+        const void *fl = (const void *)lookup512_pipe_kernel;
+        const unsigned g = grid_for(fl, kTPB, 0, (n + kTPB - 1) / kTPB);
+        return launch_words(lookup512_pipe_kernel, g, p, words, s, p, (const u64 *)words, keys,
+                            n, out, hits);
+    }
     if (OP == OP_CONTAINS && p.fast_random) {
         const void *fl = (const void *)lookup512_kernel<C>;
         const unsigned g = grid_for(fl, kTPB, 0, (n + kTPB - 1) / kTPB);
-        lookup512_kernel<C><<<g, kTPB, 0, s>>>(p, words, keys, n, out, hits);
-        count_launch();
-        return cudaGetLastError();
+        return launch_words(lookup512_kernel<C>, g, p, words, s, p, (const u64 *)words, keys, n,
+                            out, hits);
     }
     const void *fn = (const void *)blocks512_kernel<OP, C>;
     unsigned grid = grid_for(fn, kTPB, 0, (n + kTPB - 1) / kTPB);
     if (p.max_ctas && grid > p.max_ctas) grid = p.max_ctas;
-    blocks512_kernel<OP, C><<<grid, kTPB, 0, s>>>(p, words, keys, n, out, hits);
-    count_launch();
-    return cudaGetLastError();
+    return launch_words(blocks512_kernel<OP, C>, grid, p, words, s, p, words, keys, n, out, hits);
 }
 
 template <int OP>

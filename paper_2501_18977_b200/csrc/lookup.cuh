@@ -73,4 +73,44 @@ __device__ __forceinline__ bool lookup_tile(const KParams &p, const u64 *__restr
     return found;
 }
 
+// ---- single choice, software-pipelined ---------------------------------------------
+// With one choice there is no early exit to wait for, so a warp can keep two
+// tiles in flight: the block fetch of tile t+1 (one cp.async group into the
+// other stage) is outstanding while tile t is tested.  Block numbers reach the
+// copying lanes by shuffle instead of a shared-memory round trip.
+struct PipeStage {
+    uint4 blocks[32][4];
+};
+
+__device__ __forceinline__ void stage_blocks(const u64 *__restrict__ words, PipeStage &st,
+                                             u32 blk, u32 live, int lane) {
+    const int g = lane >> 2, s = lane & 3;
+    const uint4 *w4 = reinterpret_cast<const uint4 *>(words);
+#pragma unroll
+    for (int pp = 0; pp < 4; ++pp) {
+        const int kk = 4 * g + pp;
+        const u32 b = __shfl_sync(0xffffffffu, blk, kk);
+        if ((live >> kk) & 1u) {
+            const u32 dst = (u32)__cvta_generic_to_shared(&st.blocks[stage_row(kk)][s]);
+            asm volatile("cp.async.cg.shared.global.L2::64B [%0], [%1], 16;" ::"r"(dst),
+                         "l"(w4 + (u64)b * 4 + s));
+        }
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+}
+
+// All k bits of key x set in this lane's staged block?
+__device__ __forceinline__ bool test_staged(const KParams &p, const PipeStage &st, u64 x,
+                                            int lane) {
+    const u32 xlo = (u32)x, xhi = (u32)(x >> 32);
+    const u32 *mine = reinterpret_cast<const u32 *>(&st.blocks[stage_row(lane)][0]);
+    u32 acc = 1u;
+#pragma unroll 4
+    for (u32 i = 0; i < p.k; ++i) {
+        const u32 h = bit512(p.bit_a_lo[i], p.bit_a_hi[i], xlo, xhi);
+        acc &= mine[h >> 5] >> (h & 31);
+    }
+    return (acc & 1u) != 0u;
+}
+
 }  // namespace bc
