@@ -173,6 +173,12 @@ BC_API unsigned long long bc_launch_count(void);
 /* Library version string. */
 BC_API const char *bc_version(void);
 
+/* Filters that fit in L2 are launched with their words marked L2-persisting
+ * (BC_L2_PERSIST=0 disables).  This demotes the persisting lines and returns
+ * the set-aside on the current device; call it at teardown (the Python layer
+ * does so at exit).  Launches that do not use the window call it themselves. */
+BC_API void bc_l2_release(void);
+
 #ifdef __cplusplus
 }
 #endif

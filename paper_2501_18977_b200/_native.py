@@ -7,12 +7,14 @@ or a CUDA device is missing, every batched operation raises.
 
 from __future__ import annotations
 
+import atexit
 import ctypes
 import os
 import threading
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libbbchoc.so")
+# BC_LIBRARY: load another build of the same ABI (A/B measurements)
+LIB_PATH = os.environ.get("BC_LIBRARY") or os.path.join(HERE, "libbbchoc.so")
 
 BC_OK, BC_EINVAL, BC_ECUDA, BC_ENOMEM, BC_EUNSUP = 0, -1, -2, -3, -4
 BC_INSERT_ORDERED, BC_INSERT_RELAXED = 0, 1
@@ -23,7 +25,7 @@ EXPORTS = (
     "bc_filter_create", "bc_filter_destroy", "bc_insert", "bc_contains",
     "bc_insert_host", "bc_contains_host", "bc_encode_qgrams", "bc_insert_qgrams",
     "bc_contains_qgrams", "bc_block_histogram", "bc_route", "bc_eval_hash",
-    "bc_last_error", "bc_launch_count", "bc_version", "bc_pcg64_fill",
+    "bc_last_error", "bc_launch_count", "bc_version", "bc_pcg64_fill", "bc_l2_release",
 )
 
 
@@ -88,6 +90,7 @@ def lib() -> ctypes.CDLL:
         L.bc_last_error.restype = ctypes.c_char_p
         L.bc_launch_count.restype = ctypes.c_ulonglong
         L.bc_version.restype = ctypes.c_char_p
+        L.bc_l2_release.restype = None
         for name in EXPORTS:
             fn = getattr(L, name)
             if fn.restype is ctypes.c_int or name in (
@@ -97,6 +100,7 @@ def lib() -> ctypes.CDLL:
                     "bc_pcg64_fill"):
                 fn.restype = ctypes.c_int
         _lib = L
+        atexit.register(L.bc_l2_release)
         return L
 
 

@@ -61,8 +61,10 @@ __device__ __forceinline__ void phase1(const KParams &p, u64 x, bool valid, Warp
             const u32 xlo = (u32)x, xhi = (u32)(x >> 32);
 #pragma unroll 4
             for (u32 i = 0; i < p.k; ++i) {
-                u32 h = bit512(p.bit_a_lo[i], p.bit_a_hi[i], xlo, xhi);
-                col[(h >> 5) * 32] |= 1u << (h & 31);
+                const u32 hi = mul_hi32(p.bit_a_lo[i], p.bit_a_hi[i], xlo, xhi);
+                // bit (hi >> 23) & 31 of word hi >> 28; one shared-memory atomic
+                // instead of a load / or / store chain (each lane owns its column)
+                atomicOr(&col[(hi >> 28) * 32], __funnelshift_l(0u, 1u, hi >> 23));
             }
         } else if (p.strategy == 0) {
             for (u32 i = 0; i < p.k; ++i) {

@@ -74,9 +74,12 @@ __device__ __forceinline__ u64 block_index(const KParams &p, u64 x, int ci) {
 
 // Top 9 bits of the low 64 bits of a*x: the SHIFT_POW2 hash with B = 512
 // (s = 55), computed from 32-bit halves with three IMADs.
+__device__ __forceinline__ u32 mul_hi32(u32 alo, u32 ahi, u32 xlo, u32 xhi) {
+    return __umulhi(alo, xlo) + alo * xhi + ahi * xlo;  // bits 32..63 of a*x
+}
+
 __device__ __forceinline__ u32 bit512(u32 alo, u32 ahi, u32 xlo, u32 xhi) {
-    u32 hi = __umulhi(alo, xlo) + alo * xhi + ahi * xlo;
-    return hi >> 23;
+    return mul_hi32(alo, ahi, xlo, xhi) >> 23;
 }
 
 // Position of the r-th (0-based) set bit of v (requires r < popc(v)).

@@ -128,6 +128,7 @@ __global__ void __launch_bounds__(kTPB) lookup512_kernel(const __grid_constant__
 }
 
 // Single-choice lookups with two tiles per warp in flight (lookup.cuh).
+template <int K>
 __global__ void __launch_bounds__(kTPB) lookup512_pipe_kernel(const __grid_constant__ KParams p,
                                                               const u64 *__restrict__ words,
                                                               const u64 *__restrict__ keys, u64 n,
@@ -158,7 +159,7 @@ __global__ void __launch_bounds__(kTPB) lookup512_pipe_kernel(const __grid_const
         const u64 x_nn = i < n ? ld_stream(keys + i) : 0ull;
         asm volatile("cp.async.wait_group 1;" ::: "memory");
         __syncwarp();
-        const bool f = valid && test_staged(p, st[b], x, lane);
+        const bool f = valid && test_staged<K>(p, st[b], x, lane);
         if (out != nullptr && valid) out[base + lane] = (u8)f;
         my_hits += f ? 1u : 0u;
         __syncwarp();
@@ -373,9 +374,11 @@ static const L2Info &l2_info() {
         if (cudaDeviceGetAttribute(&v, cudaDevAttrL2CacheSize, dev) == cudaSuccess) i.l2 = v;
         if (cudaDeviceGetAttribute(&v, cudaDevAttrMaxAccessPolicyWindowSize, dev) == cudaSuccess)
             i.window = v;
-        if (cudaDeviceGetAttribute(&v, cudaDevAttrMaxPersistingL2CacheSize, dev) == cudaSuccess &&
-            v > 0 && cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, (size_t)v) == cudaSuccess)
-            i.persist = v;
+        if (cudaDeviceGetAttribute(&v, cudaDevAttrMaxPersistingL2CacheSize, dev) == cudaSuccess)
+            i.persist = v > 0 ? v : 0;
+        // lines left persisting by an earlier process would shrink the L2
+        // for everything this one does
+        cudaCtxResetPersistingL2Cache();
         cudaGetLastError();
         return i;
     }();
@@ -390,14 +393,31 @@ static int l2_persist_mode() {  // -1 auto, 0 off, 1 forced
     return m;
 }
 
-static std::atomic<bool> g_l2_used{false};
+// The persisting set-aside is carved out only while windows are in use: it and
+// the persisting lines are given back (reset + limit 0) by the first launch
+// that runs without a window, by filter teardown and at exit (bc_l2_release).
+static std::mutex g_l2_mu;
+static bool g_l2_on = false;
+
+static bool l2_acquire() {
+    std::lock_guard<std::mutex> lk(g_l2_mu);
+    if (!g_l2_on) {
+        if (cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, l2_info().persist) != cudaSuccess) {
+            cudaGetLastError();
+            return false;
+        }
+        g_l2_on = true;
+    }
+    return true;
+}
 
 void l2_release() {
-    // persisting lines outlive the launches (and the process's other work
-    // competes with them): demote them to normal when a filter is destroyed
-    if (g_l2_used.exchange(false)) {
+    std::lock_guard<std::mutex> lk(g_l2_mu);
+    if (g_l2_on) {
         cudaCtxResetPersistingL2Cache();
+        cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, 0);
         cudaGetLastError();
+        g_l2_on = false;
     }
 }
 
@@ -413,7 +433,10 @@ static cudaError_t launch_words(K kernel, unsigned grid, const KParams &p, const
     const size_t fbytes = (size_t)p.num_blocks * p.wpb * 8;
     const int mode = l2_persist_mode();
     const L2Info &li = l2_info();
-    if (mode != 0 && li.persist && li.window && (mode == 1 || fbytes <= li.l2)) {
+    const bool want = mode != 0 && li.persist && li.window && (mode == 1 || fbytes <= li.l2);
+    if (!want) {
+        l2_release();
+    } else if (l2_acquire()) {
         const size_t bytes = std::min(fbytes, li.window);
         attr[0].id = cudaLaunchAttributeAccessPolicyWindow;
         attr[0].val.accessPolicyWindow.base_ptr = const_cast<u64 *>(words);
@@ -424,20 +447,38 @@ static cudaError_t launch_words(K kernel, unsigned grid, const KParams &p, const
         attr[0].val.accessPolicyWindow.missProp = cudaAccessPropertyNormal;
         cfg.attrs = attr;
         cfg.numAttrs = 1;
-        g_l2_used.store(true, std::memory_order_relaxed);
     }
     count_launch();
     return cudaLaunchKernelEx(&cfg, kernel, args...);
+}
+
+template <int K>
+static cudaError_t launch_pipe_k(const KParams &p, const u64 *words, const u64 *keys, u64 n,
+                                 u8 *out, unsigned long long *hits, cudaStream_t s) {
+    const void *fl = (const void *)lookup512_pipe_kernel<K>;
+    const unsigned g = grid_for(fl, kTPB, 0, (n + kTPB - 1) / kTPB);
+    return launch_words(lookup512_pipe_kernel<K>, g, p, words, s, p, words, keys, n, out, hits);
+}
+
+// k known at compile time for the common 4..16 (fully unrolled bit tests)
+static cudaError_t launch_pipe(const KParams &p, const u64 *words, const u64 *keys, u64 n,
+                               u8 *out, unsigned long long *hits, cudaStream_t s) {
+    switch (p.k) {
+#define BC_PIPE_K(k) \
+    case k: return launch_pipe_k<k>(p, words, keys, n, out, hits, s);
+        BC_PIPE_K(4) BC_PIPE_K(5) BC_PIPE_K(6) BC_PIPE_K(7) BC_PIPE_K(8) BC_PIPE_K(9)
+        BC_PIPE_K(10) BC_PIPE_K(11) BC_PIPE_K(12) BC_PIPE_K(13) BC_PIPE_K(14) BC_PIPE_K(15)
+        BC_PIPE_K(16)
+#undef BC_PIPE_K
+        default: return launch_pipe_k<0>(p, words, keys, n, out, hits, s);
+    }
 }
 
 template <int OP, int C>
 static cudaError_t launch512(const KParams &p, u64 *words, const u64 *keys, u64 n, u8 *out,
                              unsigned long long *hits, cudaStream_t s) {
     if (OP == OP_CONTAINS && p.fast_random && C == 1 && lookup_pipe_enabled()) {
-        const void *fl = (const void *)lookup512_pipe_kernel;
-        const unsigned g = grid_for(fl, kTPB, 0, (n + kTPB - 1) / kTPB);
-        return launch_words(lookup512_pipe_kernel, g, p, words, s, p, (const u64 *)words, keys,
-                            n, out, hits);
+        return launch_pipe(p, words, keys, n, out, hits, s);
     }
     if (OP == OP_CONTAINS && p.fast_random) {
         const void *fl = (const void *)lookup512_kernel<C>;
@@ -474,6 +515,7 @@ cudaError_t launch_blocks(int op, const KParams &p, u64 *words, const u64 *keys,
         return op == OP_CONTAINS ? launch512_c<OP_CONTAINS>(p, words, keys, n, out, hits, s)
                                  : launch512_c<OP_INSERT>(p, words, keys, n, out, hits, s);
     }
+    l2_release();
     const void *fn = op == OP_CONTAINS ? (const void *)generic_kernel<OP_CONTAINS>
                                        : (const void *)generic_kernel<OP_INSERT>;
     unsigned grid = grid_for(fn, 256, 0, (n + 255) / 256);
@@ -489,6 +531,7 @@ cudaError_t launch_blocks(int op, const KParams &p, u64 *words, const u64 *keys,
 cudaError_t launch_ordered(const KParams &p, u64 *words, const u64 *keys, u64 n, u64 chunk,
                            u64 *owner, u32 *lists, u32 *state, cudaStream_t s) {
     if (n == 0) return cudaSuccess;
+    l2_release();
     const void *fn = (const void *)ordered_kernel;
     const unsigned grid = grid_for(fn, 256, 0, (chunk + 255) / 256);
     KParams pp = p;
@@ -502,6 +545,7 @@ cudaError_t launch_ordered(const KParams &p, u64 *words, const u64 *keys, u64 n,
 cudaError_t launch_flat(int op, const KParams &p, u64 *words, const u64 *keys, u64 n, u8 *out,
                         unsigned long long *hits, cudaStream_t s) {
     if (n == 0) return cudaSuccess;
+    l2_release();
     const void *fn = op == OP_CONTAINS ? (const void *)flat_kernel<OP_CONTAINS>
                                        : (const void *)flat_kernel<OP_INSERT>;
     const unsigned grid = grid_for(fn, 256, 0, (n + 255) / 256);

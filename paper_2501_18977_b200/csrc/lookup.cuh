@@ -99,16 +99,29 @@ __device__ __forceinline__ void stage_blocks(const u64 *__restrict__ words, Pipe
     asm volatile("cp.async.commit_group;" ::: "memory");
 }
 
-// All k bits of key x set in this lane's staged block?
+// Bit h = hi >> 23 of the staged block, moved to bit 0: word hi >> 28 rotated
+// right by (hi >> 23) & 31 (the funnel shift's wrap mode does the & 31).
+__device__ __forceinline__ u32 staged_bit(const u32 *mine, u32 hi) {
+    const u32 w = mine[hi >> 28];
+    return __funnelshift_r(w, w, hi >> 23);
+}
+
+// All k bits of key x set in this lane's staged block?  K > 0: k known at
+// compile time (fully unrolled); K == 0: runtime k.
+template <int K>
 __device__ __forceinline__ bool test_staged(const KParams &p, const PipeStage &st, u64 x,
                                             int lane) {
     const u32 xlo = (u32)x, xhi = (u32)(x >> 32);
     const u32 *mine = reinterpret_cast<const u32 *>(&st.blocks[stage_row(lane)][0]);
     u32 acc = 1u;
+    if (K > 0) {
+#pragma unroll
+        for (int i = 0; i < K; ++i)
+            acc &= staged_bit(mine, mul_hi32(p.bit_a_lo[i], p.bit_a_hi[i], xlo, xhi));
+    } else {
 #pragma unroll 4
-    for (u32 i = 0; i < p.k; ++i) {
-        const u32 h = bit512(p.bit_a_lo[i], p.bit_a_hi[i], xlo, xhi);
-        acc &= mine[h >> 5] >> (h & 31);
+        for (u32 i = 0; i < p.k; ++i)
+            acc &= staged_bit(mine, mul_hi32(p.bit_a_lo[i], p.bit_a_hi[i], xlo, xhi));
     }
     return (acc & 1u) != 0u;
 }

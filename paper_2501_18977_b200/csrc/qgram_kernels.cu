@@ -318,6 +318,7 @@ cudaError_t launch_qgram_blocks(int op, const KParams &p, u64 *words, const u8 *
                                 unsigned long long *hits, unsigned long long *count,
                                 cudaStream_t s) {
     if (p.wpb != 8) return cudaErrorInvalidValue;  // caller falls back to encode + array path
+    l2_release();
     return op == OP_CONTAINS ? launch_qb_c<OP_CONTAINS>(p, words, seq, len, q, canonical,
                                                         tile_off, out, hits, count, s)
                              : launch_qb_c<OP_INSERT>(p, words, seq, len, q, canonical,
