@@ -64,7 +64,11 @@ __device__ __forceinline__ void phase1(const KParams &p, u64 x, bool valid, Warp
                 const u32 hi = mul_hi32(p.bit_a_lo[i], p.bit_a_hi[i], xlo, xhi);
                 // bit (hi >> 23) & 31 of word hi >> 28; one shared-memory atomic
                 // instead of a load / or / store chain (each lane owns its column)
+#ifdef BC_PHASE1_RMW
+                col[(hi >> 28) * 32] |= __funnelshift_l(0u, 1u, hi >> 23);
+#else
                 atomicOr(&col[(hi >> 28) * 32], __funnelshift_l(0u, 1u, hi >> 23));
+#endif
             }
         } else if (p.strategy == 0) {
             for (u32 i = 0; i < p.k; ++i) {

@@ -95,7 +95,7 @@ __global__ void __launch_bounds__(kTPB) blocks512_kernel(const __grid_constant__
 
 // Lookups, 512-bit blocks, random strategy: staged blocks + per-address test
 // (lookup.cuh), early exit over the choices.
-template <int C>
+template <int C, int K>
 __global__ void __launch_bounds__(kTPB) lookup512_kernel(const __grid_constant__ KParams p,
                                                          const u64 *__restrict__ words,
                                                          const u64 *__restrict__ keys, u64 n,
@@ -116,7 +116,7 @@ __global__ void __launch_bounds__(kTPB) lookup512_kernel(const __grid_constant__
         const u64 x = x_next;
         const u64 nb = base + nwarps * 32 + lane;
         x_next = nb < n ? ld_stream(keys + nb) : 0ull;
-        const bool f = lookup_tile<C>(p, words, ls, x, valid, lane);
+        const bool f = lookup_tile<C, K>(p, words, ls, x, valid, lane);
         if (out != nullptr && valid) out[base + lane] = (u8)f;
         my_hits += f ? 1u : 0u;
         __syncwarp();
@@ -474,6 +474,32 @@ static cudaError_t launch_pipe(const KParams &p, const u64 *words, const u64 *ke
     }
 }
 
+template <int C, int K>
+static cudaError_t launch_lookup_k(const KParams &p, const u64 *words, const u64 *keys, u64 n,
+                                   u8 *out, unsigned long long *hits, cudaStream_t s) {
+    const void *fl = (const void *)lookup512_kernel<C, K>;
+    const unsigned g = grid_for(fl, kTPB, 0, (n + kTPB - 1) / kTPB);
+    return launch_words(lookup512_kernel<C, K>, g, p, words, s, p, words, keys, n, out, hits);
+}
+
+// multi-choice lookups: compile-time k for two and three choices
+template <int C>
+static cudaError_t launch_lookup(const KParams &p, const u64 *words, const u64 *keys, u64 n,
+                                 u8 *out, unsigned long long *hits, cudaStream_t s) {
+    if (C <= 3) {
+        switch (p.k) {
+#define BC_LOOKUP_K(k) \
+    case k: return launch_lookup_k<C, (C <= 3 ? k : 0)>(p, words, keys, n, out, hits, s);
+            BC_LOOKUP_K(4) BC_LOOKUP_K(5) BC_LOOKUP_K(6) BC_LOOKUP_K(7) BC_LOOKUP_K(8)
+            BC_LOOKUP_K(9) BC_LOOKUP_K(10) BC_LOOKUP_K(11) BC_LOOKUP_K(12) BC_LOOKUP_K(13)
+            BC_LOOKUP_K(14) BC_LOOKUP_K(15) BC_LOOKUP_K(16)
+#undef BC_LOOKUP_K
+            default: break;
+        }
+    }
+    return launch_lookup_k<C, 0>(p, words, keys, n, out, hits, s);
+}
+
 template <int OP, int C>
 static cudaError_t launch512(const KParams &p, u64 *words, const u64 *keys, u64 n, u8 *out,
                              unsigned long long *hits, cudaStream_t s) {
@@ -481,10 +507,7 @@ static cudaError_t launch512(const KParams &p, u64 *words, const u64 *keys, u64 
         return launch_pipe(p, words, keys, n, out, hits, s);
     }
     if (OP == OP_CONTAINS && p.fast_random) {
-        const void *fl = (const void *)lookup512_kernel<C>;
-        const unsigned g = grid_for(fl, kTPB, 0, (n + kTPB - 1) / kTPB);
-        return launch_words(lookup512_kernel<C>, g, p, words, s, p, (const u64 *)words, keys, n,
-                            out, hits);
+        return launch_lookup<C>(p, words, keys, n, out, hits, s);
     }
     const void *fn = (const void *)blocks512_kernel<OP, C>;
     unsigned grid = grid_for(fn, kTPB, 0, (n + kTPB - 1) / kTPB);

@@ -30,7 +30,9 @@ struct LookupSmem {
 // different bank halves, so the staging stores are conflict-free.
 __device__ __forceinline__ int stage_row(int kk) { return kk ^ ((kk >> 2) & 1); }
 
-template <int C>
+__device__ __forceinline__ u32 staged_bit(const u32 *mine, u32 hi);
+
+template <int C, int K = 0>
 __device__ __forceinline__ bool lookup_tile(const KParams &p, const u64 *__restrict__ words,
                                             LookupSmem<C> &ls, u64 x, bool valid, int lane) {
     constexpr u32 full = 0xffffffffu;
@@ -61,10 +63,14 @@ __device__ __forceinline__ bool lookup_tile(const KParams &p, const u64 *__restr
         __syncwarp();
         if (!((done >> lane) & 1u)) {
             u32 acc = 1u;
+            if (K > 0) {
+#pragma unroll
+                for (int i = 0; i < K; ++i)
+                    acc &= staged_bit(mine, mul_hi32(p.bit_a_lo[i], p.bit_a_hi[i], xlo, xhi));
+            } else {
 #pragma unroll 4
-            for (u32 i = 0; i < p.k; ++i) {
-                const u32 h = bit512(p.bit_a_lo[i], p.bit_a_hi[i], xlo, xhi);
-                acc &= mine[h >> 5] >> (h & 31);
+                for (u32 i = 0; i < p.k; ++i)
+                    acc &= staged_bit(mine, mul_hi32(p.bit_a_lo[i], p.bit_a_hi[i], xlo, xhi));
             }
             found = (acc & 1u) != 0u;
         }

@@ -127,6 +127,27 @@ def test_lookups_on_oracle_built_words_are_bit_identical():
         np.testing.assert_array_equal(f.contains_many(probes), o.contains_many(probes))
 
 
+@pytest.mark.parametrize("kind,c,k,shards", [
+    ("blocked", 1, 1, 1), ("blocked", 1, 3, 1), ("blocked", 1, 4, 1), ("blocked", 1, 9, 4),
+    ("blocked", 1, 16, 1), ("blocked", 1, 17, 1), ("blocked", 1, 24, 2), ("blocked", 1, 40, 1),
+    ("blowchoc", 2, 3, 1), ("blowchoc", 2, 11, 2), ("blowchoc", 4, 20, 1),
+])
+def test_lookup_kernels_every_k(kind, c, k, shards):
+    """Inserts and lookups over the k range: compile-time-k lookup kernels
+    (4 <= k <= 16), the runtime-k fallback and sharded layouts, against the
+    oracle on the same seeded keys; ragged batch tails included."""
+    n = 3 * 2**13 + 5
+    o = orc.make_filter(kind, k=k, choices=c, size_bits=k * n, seed=7 + k, shards=shards)
+    keys = orc.even_keys(n, 8)
+    o.insert_many(keys)
+    f = bb.Filter.from_config(bb.FilterConfig(kind=kind, k=k, choices=c, size_bits=k * n,
+                                              seed=7 + k, shards=shards))
+    f.insert_many(keys)
+    np.testing.assert_array_equal(f.storage.words, o.words)
+    probes = np.concatenate([keys[::3], orc.odd_keys(2**16 + 3, 9)])
+    np.testing.assert_array_equal(f.contains_many(probes), o.contains_many(probes))
+
+
 def test_cfg2_full_size_bit_identical():
     """BASELINE config 2 at full size: 2^26 keys, k=12, 12 bits/key; the GPU
     bit array equals the oracle's (threaded OR build, itself pinned to the
