@@ -164,6 +164,12 @@ BC_API int bc_pcg64_fill(uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi, 
                          uint64_t offset, uint64_t n, uint64_t and_mask, uint64_t or_mask,
                          uint64_t *d_out, void *stream);
 
+/* Host-side query output of the CLI (cli.py:141-142): writes one line
+ * "<decimal key>\t<0|1>\n" per key into h_out (at most 23 * n bytes, which
+ * out_cap must cover) and stores the byte count in *written. */
+BC_API int bc_format_answers(const uint64_t *h_keys, const uint8_t *h_answers, uint64_t n,
+                             char *h_out, uint64_t out_cap, uint64_t *written);
+
 /* Thread-local description of the last error on this thread. */
 BC_API const char *bc_last_error(void);
 

@@ -536,6 +536,51 @@ extern "C" int bc_pcg64_fill(uint64_t state_hi, uint64_t state_lo, uint64_t inc_
     return BC_OK;
 }
 
+// ---- CLI query output -----------------------------------------------------------------
+extern "C" int bc_format_answers(const uint64_t *h_keys, const uint8_t *h_answers, uint64_t n,
+                                 char *h_out, uint64_t out_cap, uint64_t *written) {
+    if (!written) return fail(BC_EINVAL, "null byte count");
+    *written = 0;
+    if (n == 0) return BC_OK;
+    if (!h_keys || !h_answers || !h_out) return fail(BC_EINVAL, "null keys, answers or output");
+    if (out_cap / 23 < n) return fail(BC_EINVAL, "output buffer below 23 bytes per key");
+    static const struct Pairs {
+        char d[200];
+        Pairs() {
+            for (int i = 0; i < 100; ++i) {
+                d[2 * i] = (char)('0' + i / 10);
+                d[2 * i + 1] = (char)('0' + i % 10);
+            }
+        }
+    } pairs;
+    char *o = h_out;
+    for (uint64_t i = 0; i < n; ++i) {
+        uint64_t v = h_keys[i];
+        char buf[20];
+        int p = 20;
+        while (v >= 100) {
+            const unsigned r = (unsigned)(v % 100);
+            v /= 100;
+            p -= 2;
+            std::memcpy(buf + p, pairs.d + 2 * r, 2);
+        }
+        if (v >= 10) {
+            p -= 2;
+            std::memcpy(buf + p, pairs.d + 2 * v, 2);
+        } else {
+            buf[--p] = (char)('0' + v);
+        }
+        std::memcpy(o, buf + p, 20 - p);
+        o += 20 - p;
+        o[0] = '\t';
+        o[1] = h_answers[i] ? '1' : '0';
+        o[2] = '\n';
+        o += 3;
+    }
+    *written = (uint64_t)(o - h_out);
+    return BC_OK;
+}
+
 // ---- host-buffer entry points ---------------------------------------------------------
 // Per-device staging: two pinned key buffers, two pinned answer buffers, two
 // device key/answer buffers and two copy streams, so the copy of chunk i+1
