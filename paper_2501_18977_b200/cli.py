@@ -25,7 +25,9 @@ import numpy as np
 from ._native import check, lib
 from .analysis import block_load_histogram, estimate_fpr
 from .filters import GOLDEN_BETA, ConfigError, CostModel, Filter, FilterConfig
-from .io import FilterFormatError, KeyFormatError, read_filter, read_keys, write_filter
+from .io import (FilterFormatError, KeyFormatError, fasta_batches, read_filter, read_keys,
+                 write_filter)
+from .qgrams import QGramEncoder
 from .sharding import build_sharded
 
 EXIT_OK = 0
@@ -110,7 +112,17 @@ def _key_stream(args):
 def cmd_build(args) -> int:
     config = _make_config(args)
     t0 = time.perf_counter()
-    filt = build_sharded(config, _key_stream(args))
+    if args.format == "fasta":
+        # FASTA: batches of whole records straight into the fused q-gram
+        # insert (== inserting encode_qgrams of each record in order)
+        if args.q is None:
+            raise KeyFormatError("FASTA input needs a q-gram length")
+        enc = QGramEncoder(q=args.q, canonical=not args.no_canonical)
+        filt = Filter.from_config(config.validated())
+        for batch in fasta_batches(args.keys):
+            filt.insert_qgrams(enc, batch)
+    else:
+        filt = build_sharded(config, _key_stream(args))
     wall = time.perf_counter() - t0
     write_filter(filt, args.out)
     print(_tsv("keys_inserted", "load", "wall_s", "m_bits", "blocks", "shards"),

@@ -27,7 +27,7 @@ from typing import BinaryIO, Iterator
 import numpy as np
 
 from .filters import CostModel, Filter
-from .qgrams import QGramEncoder, encode_qgrams
+from .qgrams import QGramEncoder, encode_qgrams, join_records
 
 MAGIC = b"BWCH"
 FORMAT_VERSION = 1
@@ -196,6 +196,27 @@ def fasta_records(fh: BinaryIO) -> Iterator[bytes]:
             parts.append(line)
     if parts:
         yield b"".join(parts)
+
+
+def fasta_batches(path, batch_bytes: int = 1 << 28) -> Iterator[bytes]:
+    """FASTA records joined (join_records) into batches of about batch_bytes,
+    for the fused q-gram kernels: the windows of a batch are those of its
+    records, in order, and none spans two records."""
+    fh = _open_binary(path)
+    try:
+        batch: list = []
+        size = 0
+        for rec in fasta_records(fh):
+            batch.append(rec)
+            size += len(rec) + 1
+            if size >= batch_bytes:
+                yield join_records(batch)
+                batch, size = [], 0
+        if batch:
+            yield join_records(batch)
+    finally:
+        if fh is not sys.stdin.buffer:
+            fh.close()
 
 
 def read_keys(path, fmt: str, *, q: int | None = None, canonical: bool = True,

@@ -152,3 +152,42 @@ def test_build_query_hist_fpr_end_to_end(kind, c, threads, tmp_path):
         lines = r.stdout.decode().strip().splitlines()
         counts = np.array([int(x.split("\t")[1]) for x in lines[1:]])
         np.testing.assert_array_equal(counts, ref.block_histogram())
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("canonical", [True, False])
+def test_fasta_build_fused_equals_record_stream(canonical, tmp_path):
+    """build --format fasta runs the fused q-gram insert over batches of whole
+    records; the words equal the oracle's insert of each record's q-grams in
+    record order (c = 2, ordered), and query prints every window's key."""
+    rng = np.random.default_rng(5)
+    recs = []
+    for i in range(7):
+        seq = bytearray(rng.choice(np.frombuffer(b"ACGTacgt", np.uint8),
+                                    size=int(rng.integers(5, 4000))).tobytes())
+        for p in rng.integers(0, len(seq), size=3):
+            seq[p] = ord("N")
+        recs.append(bytes(seq))
+    fa = tmp_path / "r.fa"
+    fa.write_bytes(b"".join(b">r%d\n" % i + r[:60] + b"\n" + r[60:] + b"\n"
+                            for i, r in enumerate(recs)))
+    q, k = 21, 8
+    keys = np.concatenate([orc.encode_qgrams(r, q, canonical) for r in recs])
+    out = tmp_path / "f.bwch"
+    args = ["build", "--kind", "blowchoc", "--k", k, "--choices", 2, "--n", keys.size,
+            "--seed", 3, "--keys", fa, "--format", "fasta", "--q", q, "--out", out]
+    if not canonical:
+        args.append("--no-canonical")
+    r = run_cli(*args)
+    assert r.returncode == 0, r.stderr.decode()
+    ref = orc.make_filter("blowchoc", k=k, choices=2, n_capacity=keys.size, seed=3)
+    ref.insert_many(keys)
+    o, inserted = oracle_of(out)
+    assert inserted == keys.size
+    np.testing.assert_array_equal(o.words, ref.words)
+    qargs = ["query", "--filter", out, "--keys", fa, "--format", "fasta", "--q", q]
+    if not canonical:
+        qargs.append("--no-canonical")
+    r = run_cli(*qargs)
+    assert r.returncode == 0, r.stderr.decode()
+    assert r.stdout == expected_tsv(keys, np.ones(keys.size, dtype=bool))
