@@ -127,6 +127,28 @@ def test_u64le_and_text_streams(tmp_path):
         list(read_keys(str(t), "fasta"))
 
 
+def test_fasta_batches_keep_records_whole_and_in_order(tmp_path):
+    from paper_2501_18977_b200.io import fasta_batches, fasta_records
+
+    recs = [b"ACGT" * 5, b"GGCA", b"", b"T" * 30, b"acgtN" * 3]
+    fa = tmp_path / "r.fa"
+    fa.write_bytes(b"".join(b">h%d desc\n" % i + r[:7] + b"\n" + r[7:] + b"\n"
+                            for i, r in enumerate(recs)))
+    with open(fa, "rb") as fh:
+        kept = list(fasta_records(fh))
+    assert kept == [r for r in recs if r]
+    for size in (1, 25, 10**6):
+        batches = list(fasta_batches(str(fa), batch_bytes=size))
+        # joined with a non-ACGT separator: same windows as the records
+        assert b"\n".join(batches) == bb.join_records(kept)
+        assert all(b.count(b">") == 0 for b in batches)
+    assert len(list(fasta_batches(str(fa), batch_bytes=1))) == len(kept)
+    bad = tmp_path / "bad.fa"
+    bad.write_bytes(b"ACGT\n>h\nACGT\n")
+    with pytest.raises(KeyFormatError):
+        list(fasta_batches(str(bad)))
+
+
 @pytest.mark.gpu
 def test_gpu_filter_roundtrip_and_fasta(tmp_path):
     from oracle import oracle as orc
