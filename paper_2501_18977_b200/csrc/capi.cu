@@ -97,7 +97,7 @@ extern "C" unsigned long long bc_launch_count(void) { return bc::launch_count();
 
 extern "C" const char *bc_version(void) { return "bbchoc-b200 0.1.0 (sm_100a)"; }
 
-extern "C" void bc_l2_release(void) { bc::l2_release(); }
+extern "C" void bc_l2_release(void) { bc::l2_release_all(); }
 
 extern "C" int bc_filter_create(const bc_filter_desc *d, bc_filter **out) {
     if (!d || !out) return fail(BC_EINVAL, "null argument");

@@ -364,25 +364,38 @@ static bool lookup_pipe_enabled() {
 // inserts: cfg3 11.9 -> 6.5 Gkeys/s).  BC_L2_PERSIST=0 disables, =1 forces.
 struct L2Info {
     size_t l2 = 0, persist = 0, window = 0;
+    bool init = false;
+    bool on = false;  // persisting set-aside carved out on this device
 };
 
-static const L2Info &l2_info() {
-    static const L2Info info = [] {
-        L2Info i;
-        int dev = 0, v = 0;
-        cudaGetDevice(&dev);
+constexpr int kMaxDevices = 64;
+static std::mutex g_l2_mu;
+static L2Info g_l2[kMaxDevices];
+
+static int current_device() {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    return dev >= 0 && dev < kMaxDevices ? dev : -1;
+}
+
+// per-device attributes; the first call on a device also resets lines left
+// persisting by an earlier process, which would shrink the L2 for everything
+// this one does.  Call with g_l2_mu held.
+static L2Info *l2_info_locked(int dev) {
+    if (dev < 0) return nullptr;
+    L2Info &i = g_l2[dev];
+    if (!i.init) {
+        int v = 0;
         if (cudaDeviceGetAttribute(&v, cudaDevAttrL2CacheSize, dev) == cudaSuccess) i.l2 = v;
         if (cudaDeviceGetAttribute(&v, cudaDevAttrMaxAccessPolicyWindowSize, dev) == cudaSuccess)
             i.window = v;
         if (cudaDeviceGetAttribute(&v, cudaDevAttrMaxPersistingL2CacheSize, dev) == cudaSuccess)
             i.persist = v > 0 ? v : 0;
-        // lines left persisting by an earlier process would shrink the L2
-        // for everything this one does
         cudaCtxResetPersistingL2Cache();
         cudaGetLastError();
-        return i;
-    }();
-    return info;
+        i.init = true;
+    }
+    return &i;
 }
 
 static int l2_persist_mode() {  // -1 auto, 0 off, 1 forced
@@ -396,29 +409,55 @@ static int l2_persist_mode() {  // -1 auto, 0 off, 1 forced
 // The persisting set-aside is carved out only while windows are in use: it and
 // the persisting lines are given back (reset + limit 0) by the first launch
 // that runs without a window, by filter teardown and at exit (bc_l2_release).
-static std::mutex g_l2_mu;
-static bool g_l2_on = false;
+static void l2_release_locked(L2Info &i) {
+    if (i.on) {
+        cudaCtxResetPersistingL2Cache();
+        cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, 0);
+        cudaGetLastError();
+        i.on = false;
+    }
+}
 
-static bool l2_acquire() {
+// Window for a filter of fbytes on the current device, or false.
+static bool l2_window(size_t fbytes, size_t *bytes, float *hit_ratio) {
+    const int mode = l2_persist_mode();
     std::lock_guard<std::mutex> lk(g_l2_mu);
-    if (!g_l2_on) {
-        if (cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, l2_info().persist) != cudaSuccess) {
+    L2Info *i = l2_info_locked(current_device());
+    if (!i) return false;
+    const bool want = mode != 0 && i->persist && i->window && (mode == 1 || fbytes <= i->l2);
+    if (!want) {
+        l2_release_locked(*i);
+        return false;
+    }
+    if (!i->on) {
+        if (cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, i->persist) != cudaSuccess) {
             cudaGetLastError();
             return false;
         }
-        g_l2_on = true;
+        i->on = true;
     }
+    *bytes = std::min(fbytes, i->window);
+    *hit_ratio = std::min(1.0f, (float)i->persist / (float)std::max<size_t>(*bytes, 1));
     return true;
 }
 
 void l2_release() {
     std::lock_guard<std::mutex> lk(g_l2_mu);
-    if (g_l2_on) {
-        cudaCtxResetPersistingL2Cache();
-        cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, 0);
-        cudaGetLastError();
-        g_l2_on = false;
+    const int dev = current_device();
+    if (dev >= 0) l2_release_locked(g_l2[dev]);
+}
+
+void l2_release_all() {
+    std::lock_guard<std::mutex> lk(g_l2_mu);
+    int prev = 0;
+    cudaGetDevice(&prev);
+    for (int d = 0; d < kMaxDevices; ++d) {
+        if (!g_l2[d].on) continue;
+        cudaSetDevice(d);
+        l2_release_locked(g_l2[d]);
     }
+    cudaSetDevice(prev);
+    cudaGetLastError();
 }
 
 template <typename K, typename... Args>
@@ -430,19 +469,13 @@ static cudaError_t launch_words(K kernel, unsigned grid, const KParams &p, const
     cfg.dynamicSmemBytes = 0;
     cfg.stream = s;
     cudaLaunchAttribute attr[1];
-    const size_t fbytes = (size_t)p.num_blocks * p.wpb * 8;
-    const int mode = l2_persist_mode();
-    const L2Info &li = l2_info();
-    const bool want = mode != 0 && li.persist && li.window && (mode == 1 || fbytes <= li.l2);
-    if (!want) {
-        l2_release();
-    } else if (l2_acquire()) {
-        const size_t bytes = std::min(fbytes, li.window);
+    size_t bytes = 0;
+    float hit = 0.f;
+    if (l2_window((size_t)p.num_blocks * p.wpb * 8, &bytes, &hit)) {
         attr[0].id = cudaLaunchAttributeAccessPolicyWindow;
         attr[0].val.accessPolicyWindow.base_ptr = const_cast<u64 *>(words);
         attr[0].val.accessPolicyWindow.num_bytes = bytes;
-        attr[0].val.accessPolicyWindow.hitRatio =
-            std::min(1.0f, (float)li.persist / (float)std::max<size_t>(bytes, 1));
+        attr[0].val.accessPolicyWindow.hitRatio = hit;
         attr[0].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
         attr[0].val.accessPolicyWindow.missProp = cudaAccessPropertyNormal;
         cfg.attrs = attr;

@@ -12,8 +12,11 @@ enum Op : int { OP_CONTAINS = 0, OP_INSERT = 1 };
 // Kernel launch accounting (bc_launch_count()).
 void count_launch(unsigned n = 1);
 
-// Demote the filter words' persisting L2 lines to normal (filter teardown).
+// Demote the filter words' persisting L2 lines to normal and give back the
+// set-aside: on the current device (teardown, launches without a window), or
+// on every device this process used (bc_l2_release).
 void l2_release();
+void l2_release_all();
 
 // Persistent-grid size: min(work_ctas, SMs x resident CTAs of `kernel`).
 unsigned grid_for(const void *kernel, int threads, size_t dyn_smem, unsigned long long work_ctas);
