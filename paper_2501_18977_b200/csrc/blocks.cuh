@@ -149,79 +149,110 @@ __device__ __forceinline__ u32 phase2(const KParams &p, u64 *words, WarpSmem<C> 
                           ws.mask[w2 + 1][kr]);
     }
     u32 found_bytes = 0;
+    if constexpr (OP == OP_INSERT && C >= 2) {
+        // Relaxed multi-choice insert, staged so the UNR keys of a step are
+        // independent work at every stage (popcounts, the two shuffle rounds,
+        // the rank loads, the REDs) instead of one dependent chain per key.
 #pragma unroll
-    for (int p0 = 0; p0 < 4; p0 += UNR) {
-        uint4 w[UNR][CL];
-        if (!kNoLoad) {
+        for (int p0 = 0; p0 < 4; p0 += UNR) {
+            uint4 w[UNR][C];
+            u32 t[UNR][C];
+#pragma unroll
+            for (int u = 0; u < UNR; ++u)
+#pragma unroll
+                for (int ci = 0; ci < C; ++ci)
+                    w[u][ci] = ld_block_cg(w4 + (u64)ws.blk[ci][4 * g + p0 + u] * 4 + s);
+#pragma unroll
+            for (int u = 0; u < UNR; ++u) {
+                const uint4 m = sel4(M, (p0 + u - s) & 3);
+#pragma unroll
+                for (int ci = 0; ci < C; ++ci) {
+                    const uint4 ww = w[u][ci];
+                    const uint4 uni = make_uint4(ww.x | m.x, ww.y | m.y, ww.z | m.z, ww.w | m.w);
+                    t[u][ci] = popc4(uni) | (popc4(ww) << 16);  // j | present << 16
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < UNR; ++u)
+#pragma unroll
+                for (int ci = 0; ci < C; ++ci) t[u][ci] += __shfl_xor_sync(kFull, t[u][ci], 1);
+#pragma unroll
+            for (int u = 0; u < UNR; ++u)
+#pragma unroll
+                for (int ci = 0; ci < C; ++ci) t[u][ci] += __shfl_xor_sync(kFull, t[u][ci], 2);
+            // a == 0 at any candidate -> no-op (_kernels.py:156-160); otherwise
+            // the strict-< argmin of the cost rank, lowest index on ties
+            u32 r[UNR][C];
+#pragma unroll
+            for (int u = 0; u < UNR; ++u)
+#pragma unroll
+                for (int ci = 0; ci < C; ++ci) {
+                    const u32 j = t[u][ci] & 0xffffu, a = j - (t[u][ci] >> 16);
+                    r[u][ci] = __ldg(p.rank + j * (p.k + 1) + a);
+                }
 #pragma unroll
             for (int u = 0; u < UNR; ++u) {
                 const int kk = 4 * g + p0 + u;
-#pragma unroll
-                for (int ci = 0; ci < C; ++ci) {
-                    const u64 b = ws.blk[ci][kk];
-                    w[u][ci] = ld_block_cg(w4 + b * 4 + s);
-                }
-            }
-        }
-#pragma unroll
-        for (int u = 0; u < UNR; ++u) {
-            const int pass = p0 + u;
-            const int kk = 4 * g + pass;
-            const uint4 m = sel4(M, (pass - s) & 3);
-            const u64 lo = (u64)m.x | ((u64)m.y << 32);
-            const u64 hi = (u64)m.z | ((u64)m.w << 32);
-            if (OP == OP_CONTAINS) {
-                bool found = false;
-#pragma unroll
-                for (int ci = 0; ci < CL; ++ci) {
-                    const u32 bal = __ballot_sync(kFull, covers(w[u][ci], m));
-                    found |= ((bal >> (lane & 28)) & 0xFu) == 0xFu;
-                }
-                found_bytes |= (found ? 1u : 0u) << (8 * pass);
-            } else if (C == 1) {
-                u64 *dst = words + (u64)ws.blk[0][kk] * 8 + s;
-                red_or(dst, lo);
-                red_or(dst + 4, hi);
-            } else {
-                u32 v[CL];
-#pragma unroll
-                for (int ci = 0; ci < CL; ++ci) {
-                    const uint4 ww = w[u][ci];
-                    const uint4 uni =
-                        make_uint4(ww.x | m.x, ww.y | m.y, ww.z | m.z, ww.w | m.w);
-                    u32 t = popc4(uni) | (popc4(ww) << 16);
-                    t += __shfl_xor_sync(kFull, t, 1);
-                    t += __shfl_xor_sync(kFull, t, 2);
-                    v[ci] = t;
-                }
+                bool noop = false;
                 int best = 0;
                 u32 best_r = 0xffffffffu;
-                bool noop = false;
 #pragma unroll
-                for (int ci = 0; ci < CL; ++ci) {
-                    if (!noop) {
-                        const u32 j = v[ci] & 0xffffu;
-                        const u32 a = j - (v[ci] >> 16);
-                        if (a == 0) {
-                            noop = true;
-                        } else {
-                            const u32 r = __ldg(p.rank + j * (p.k + 1) + a);
-                            if (r < best_r) {
-                                best_r = r;
-                                best = ci;
-                            }
-                        }
+                for (int ci = 0; ci < C; ++ci) {
+                    const u32 j = t[u][ci] & 0xffffu;
+                    noop |= j == (t[u][ci] >> 16);
+                    if (r[u][ci] < best_r) {
+                        best_r = r[u][ci];
+                        best = ci;
                     }
                 }
                 if (!noop) {
+                    const uint4 m = sel4(M, (p0 + u - s) & 3);
                     u64 *dst = words + (u64)ws.blk[best][kk] * 8 + 2 * s;
-                    red_or(dst, lo);
-                    red_or(dst + 1, hi);
+                    red_or(dst, (u64)m.x | ((u64)m.y << 32));
+                    red_or(dst + 1, (u64)m.z | ((u64)m.w << 32));
                 }
             }
         }
+        return 0;
+    } else {
+#pragma unroll
+        for (int p0 = 0; p0 < 4; p0 += UNR) {
+            uint4 w[UNR][CL];
+            if (!kNoLoad) {
+#pragma unroll
+                for (int u = 0; u < UNR; ++u) {
+                    const int kk = 4 * g + p0 + u;
+#pragma unroll
+                    for (int ci = 0; ci < C; ++ci) {
+                        const u64 b = ws.blk[ci][kk];
+                        w[u][ci] = ld_block_cg(w4 + b * 4 + s);
+                    }
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < UNR; ++u) {
+                const int pass = p0 + u;
+                const int kk = 4 * g + pass;
+                const uint4 m = sel4(M, (pass - s) & 3);
+                const u64 lo = (u64)m.x | ((u64)m.y << 32);
+                const u64 hi = (u64)m.z | ((u64)m.w << 32);
+                if (OP == OP_CONTAINS) {
+                    bool found = false;
+#pragma unroll
+                    for (int ci = 0; ci < CL; ++ci) {
+                        const u32 bal = __ballot_sync(kFull, covers(w[u][ci], m));
+                        found |= ((bal >> (lane & 28)) & 0xFu) == 0xFu;
+                    }
+                    found_bytes |= (found ? 1u : 0u) << (8 * pass);
+                } else {  // single choice: order-free OR
+                    u64 *dst = words + (u64)ws.blk[0][kk] * 8 + s;
+                    red_or(dst, lo);
+                    red_or(dst + 4, hi);
+                }
+            }
+        }
+        return found_bytes;
     }
-    return found_bytes;
 }
 
 // Write the group's four answers (keys 4g..4g+3 of a 32-key tile at `base`)
