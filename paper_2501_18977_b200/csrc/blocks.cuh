@@ -125,6 +125,97 @@ __device__ __forceinline__ uint4 sel4(const uint4 (&M)[4], int i) {
     return selp4(hi, lo, i & 2);
 }
 
+// ---- relaxed multi-choice insert steps (four lanes per key) ------------------------
+// A step covers keys 4g + p0 .. 4g + p0 + UNR - 1 of the tile: first the
+// candidate slices are loaded (relaxed_load), then (relaxed_commit) every
+// stage -- popcounts, the two shuffle rounds, the rank loads, the REDs -- runs
+// over all UNR keys at once, so the keys are independent work instead of one
+// dependent chain each.  Splitting the two lets a kernel overlap other work
+// (the next tile's phase 1) with the loads.
+constexpr int relaxed_unroll(int C) { return C <= 2 ? 4 : (C <= 4 ? 2 : 1); }
+
+template <int C, int UNR>
+__device__ __forceinline__ void relaxed_load(const WarpSmem<C> &ws, const uint4 *w4, int lane,
+                                             int p0, uint4 (&w)[UNR][C]) {
+    const int g = lane >> 2, s = lane & 3;
+#pragma unroll
+    for (int u = 0; u < UNR; ++u)
+#pragma unroll
+        for (int ci = 0; ci < C; ++ci)
+            w[u][ci] = ld_block_cg(w4 + (u64)ws.blk[ci][4 * g + p0 + u] * 4 + s);
+}
+
+template <int C, int UNR>
+__device__ __forceinline__ void relaxed_commit(const KParams &p, u64 *words,
+                                               const WarpSmem<C> &ws, const uint4 (&M)[4],
+                                               int lane, int p0, const uint4 (&w)[UNR][C]) {
+    const int g = lane >> 2, s = lane & 3;
+    u32 t[UNR][C];
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) {
+        const uint4 m = sel4(M, (p0 + u - s) & 3);
+#pragma unroll
+        for (int ci = 0; ci < C; ++ci) {
+            const uint4 ww = w[u][ci];
+            const uint4 uni = make_uint4(ww.x | m.x, ww.y | m.y, ww.z | m.z, ww.w | m.w);
+            t[u][ci] = popc4(uni) | (popc4(ww) << 16);  // j | present << 16
+        }
+    }
+#pragma unroll
+    for (int u = 0; u < UNR; ++u)
+#pragma unroll
+        for (int ci = 0; ci < C; ++ci) t[u][ci] += __shfl_xor_sync(kFull, t[u][ci], 1);
+#pragma unroll
+    for (int u = 0; u < UNR; ++u)
+#pragma unroll
+        for (int ci = 0; ci < C; ++ci) t[u][ci] += __shfl_xor_sync(kFull, t[u][ci], 2);
+    // a == 0 at any candidate -> no-op (_kernels.py:156-160); otherwise the
+    // strict-< argmin of the cost rank, lowest index on ties
+    u32 r[UNR][C];
+#pragma unroll
+    for (int u = 0; u < UNR; ++u)
+#pragma unroll
+        for (int ci = 0; ci < C; ++ci) {
+            const u32 j = t[u][ci] & 0xffffu, a = j - (t[u][ci] >> 16);
+            r[u][ci] = __ldg(p.rank + j * (p.k + 1) + a);
+        }
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) {
+        bool noop = false;
+        int best = 0;
+        u32 best_r = 0xffffffffu;
+#pragma unroll
+        for (int ci = 0; ci < C; ++ci) {
+            noop |= (t[u][ci] & 0xffffu) == (t[u][ci] >> 16);
+            if (r[u][ci] < best_r) {
+                best_r = r[u][ci];
+                best = ci;
+            }
+        }
+        if (!noop) {
+            const uint4 m = sel4(M, (p0 + u - s) & 3);
+            u64 *dst = words + (u64)ws.blk[best][4 * g + p0 + u] * 8 + 2 * s;
+            red_or(dst, (u64)m.x | ((u64)m.y << 32));
+            red_or(dst + 1, (u64)m.z | ((u64)m.w << 32));
+        }
+    }
+}
+
+// The group's mask slices for the four passes, read in rotated order (see the
+// file comment): lane s holds 64-bit words {2s, 2s+1}, or {s, s+4} (kNoLoad).
+template <int C>
+__device__ __forceinline__ void read_masks(const WarpSmem<C> &ws, int lane, bool no_load,
+                                           uint4 (&M)[4]) {
+    const int g = lane >> 2, s = lane & 3;
+    const int w0 = no_load ? 2 * s : 4 * s, w2 = no_load ? 2 * s + 8 : 4 * s + 2;
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+        const int kr = 4 * g + ((r + s) & 3);
+        M[r] = make_uint4(ws.mask[w0][kr], ws.mask[w0 + 1][kr], ws.mask[w2][kr],
+                          ws.mask[w2 + 1][kr]);
+    }
+}
+
 // ---- phase 2: four lanes per key -------------------------------------------------
 // Lookups: returns the answers of the group's four keys packed one per byte
 // (key 4g + p in byte p), identical in the four lanes of the group.
@@ -132,7 +223,7 @@ template <int OP, int C>
 __device__ __forceinline__ u32 phase2(const KParams &p, u64 *words, WarpSmem<C> &ws,
                                       int lane) {
     constexpr bool kNoLoad = (OP == OP_INSERT && C == 1);
-    constexpr int UNR = kNoLoad ? 4 : (C <= 2 ? 4 : (C <= 4 ? 2 : 1));
+    constexpr int UNR = kNoLoad ? 4 : relaxed_unroll(C);
     constexpr int CL = kNoLoad ? 1 : C;
     const int g = lane >> 2, s = lane & 3;
     const uint4 *w4 = reinterpret_cast<const uint4 *>(words);
@@ -140,78 +231,15 @@ __device__ __forceinline__ u32 phase2(const KParams &p, u64 *words, WarpSmem<C> 
     // a loaded block), or -- for single-choice inserts, which load nothing --
     // words {s, s+4}, so each of the two RED instructions of a group stays
     // inside one 32-byte sector (tools/gather_probe.cu scatter mode 6 vs 0).
-    const int w0 = kNoLoad ? 2 * s : 4 * s, w2 = kNoLoad ? 2 * s + 8 : 4 * s + 2;
     uint4 M[4];
-#pragma unroll
-    for (int r = 0; r < 4; ++r) {
-        const int kr = 4 * g + ((r + s) & 3);
-        M[r] = make_uint4(ws.mask[w0][kr], ws.mask[w0 + 1][kr], ws.mask[w2][kr],
-                          ws.mask[w2 + 1][kr]);
-    }
+    read_masks<C>(ws, lane, kNoLoad, M);
     u32 found_bytes = 0;
     if constexpr (OP == OP_INSERT && C >= 2) {
-        // Relaxed multi-choice insert, staged so the UNR keys of a step are
-        // independent work at every stage (popcounts, the two shuffle rounds,
-        // the rank loads, the REDs) instead of one dependent chain per key.
 #pragma unroll
         for (int p0 = 0; p0 < 4; p0 += UNR) {
             uint4 w[UNR][C];
-            u32 t[UNR][C];
-#pragma unroll
-            for (int u = 0; u < UNR; ++u)
-#pragma unroll
-                for (int ci = 0; ci < C; ++ci)
-                    w[u][ci] = ld_block_cg(w4 + (u64)ws.blk[ci][4 * g + p0 + u] * 4 + s);
-#pragma unroll
-            for (int u = 0; u < UNR; ++u) {
-                const uint4 m = sel4(M, (p0 + u - s) & 3);
-#pragma unroll
-                for (int ci = 0; ci < C; ++ci) {
-                    const uint4 ww = w[u][ci];
-                    const uint4 uni = make_uint4(ww.x | m.x, ww.y | m.y, ww.z | m.z, ww.w | m.w);
-                    t[u][ci] = popc4(uni) | (popc4(ww) << 16);  // j | present << 16
-                }
-            }
-#pragma unroll
-            for (int u = 0; u < UNR; ++u)
-#pragma unroll
-                for (int ci = 0; ci < C; ++ci) t[u][ci] += __shfl_xor_sync(kFull, t[u][ci], 1);
-#pragma unroll
-            for (int u = 0; u < UNR; ++u)
-#pragma unroll
-                for (int ci = 0; ci < C; ++ci) t[u][ci] += __shfl_xor_sync(kFull, t[u][ci], 2);
-            // a == 0 at any candidate -> no-op (_kernels.py:156-160); otherwise
-            // the strict-< argmin of the cost rank, lowest index on ties
-            u32 r[UNR][C];
-#pragma unroll
-            for (int u = 0; u < UNR; ++u)
-#pragma unroll
-                for (int ci = 0; ci < C; ++ci) {
-                    const u32 j = t[u][ci] & 0xffffu, a = j - (t[u][ci] >> 16);
-                    r[u][ci] = __ldg(p.rank + j * (p.k + 1) + a);
-                }
-#pragma unroll
-            for (int u = 0; u < UNR; ++u) {
-                const int kk = 4 * g + p0 + u;
-                bool noop = false;
-                int best = 0;
-                u32 best_r = 0xffffffffu;
-#pragma unroll
-                for (int ci = 0; ci < C; ++ci) {
-                    const u32 j = t[u][ci] & 0xffffu;
-                    noop |= j == (t[u][ci] >> 16);
-                    if (r[u][ci] < best_r) {
-                        best_r = r[u][ci];
-                        best = ci;
-                    }
-                }
-                if (!noop) {
-                    const uint4 m = sel4(M, (p0 + u - s) & 3);
-                    u64 *dst = words + (u64)ws.blk[best][kk] * 8 + 2 * s;
-                    red_or(dst, (u64)m.x | ((u64)m.y << 32));
-                    red_or(dst + 1, (u64)m.z | ((u64)m.w << 32));
-                }
-            }
+            relaxed_load<C, UNR>(ws, w4, lane, p0, w);
+            relaxed_commit<C, UNR>(p, words, ws, M, lane, p0, w);
         }
         return 0;
     } else {

@@ -93,6 +93,51 @@ __global__ void __launch_bounds__(kTPB) blocks512_kernel(const __grid_constant__
     }
 }
 
+// Relaxed multi-choice inserts, 512-bit blocks: the two-phase tile with the
+// next tile's phase 1 (hashing, mask build -- no filter reads, so those keys
+// are not yet in flight) issued while the current tile's candidate loads are
+// outstanding.  Double-buffered warp slices.
+template <int C>
+__global__ void __launch_bounds__(kTPB) relaxed512_kernel(const __grid_constant__ KParams p,
+                                                          u64 *__restrict__ words,
+                                                          const u64 *__restrict__ keys, u64 n) {
+    constexpr int UNR = relaxed_unroll(C);
+    __shared__ WarpSmem<C> smem[kWarps][2];
+    WarpSmem<C> *ws = smem[threadIdx.x >> 5];
+    const int lane = threadIdx.x & 31;
+    const uint4 *w4 = reinterpret_cast<const uint4 *>(words);
+    const u64 ntiles = (n + 31) / 32;
+    const u64 nwarps = (u64)gridDim.x * kWarps;
+    u64 tile = blockIdx.x * (u64)kWarps + (threadIdx.x >> 5);
+    if (tile >= ntiles) return;
+    u64 i = tile * 32 + lane;
+    phase1<C>(p, i < n ? ld_stream(keys + i) : 0ull, i < n, ws[0], lane);
+    i = (tile + nwarps) * 32 + lane;
+    u64 x_next = i < n ? ld_stream(keys + i) : 0ull;
+    int b = 0;
+    for (; tile < ntiles; tile += nwarps) {
+        __syncwarp();
+        const WarpSmem<C> &cur = ws[b];
+        uint4 M[4];
+        read_masks<C>(cur, lane, false, M);
+        uint4 w[UNR][C];
+        relaxed_load<C, UNR>(cur, w4, lane, 0, w);
+        // the next tile's phase 1 while the loads are in flight
+        const u64 nt = tile + nwarps;
+        const bool vn = nt * 32 + lane < n;
+        phase1<C>(p, x_next, vn, ws[b ^ 1], lane);
+        i = (nt + nwarps) * 32 + lane;
+        x_next = i < n ? ld_stream(keys + i) : 0ull;
+        relaxed_commit<C, UNR>(p, words, cur, M, lane, 0, w);
+#pragma unroll
+        for (int p0 = UNR; p0 < 4; p0 += UNR) {
+            relaxed_load<C, UNR>(cur, w4, lane, p0, w);
+            relaxed_commit<C, UNR>(p, words, cur, M, lane, p0, w);
+        }
+        b ^= 1;
+    }
+}
+
 // Lookups, 512-bit blocks, random strategy: staged blocks + per-address test
 // (lookup.cuh), early exit over the choices.
 template <int C, int K>
@@ -533,6 +578,14 @@ static cudaError_t launch_lookup(const KParams &p, const u64 *words, const u64 *
     return launch_lookup_k<C, 0>(p, words, keys, n, out, hits, s);
 }
 
+static bool relaxed_pipe_enabled() {  // BC_RELAXED_PIPE=0: the unpipelined tile
+    static const bool on = [] {
+        const char *e = getenv("BC_RELAXED_PIPE");
+        return e == nullptr || atoi(e) != 0;
+    }();
+    return on;
+}
+
 template <int OP, int C>
 static cudaError_t launch512(const KParams &p, u64 *words, const u64 *keys, u64 n, u8 *out,
                              unsigned long long *hits, cudaStream_t s) {
@@ -541,6 +594,14 @@ static cudaError_t launch512(const KParams &p, u64 *words, const u64 *keys, u64 
     }
     if (OP == OP_CONTAINS && p.fast_random) {
         return launch_lookup<C>(p, words, keys, n, out, hits, s);
+    }
+    // pipelined tile for 2..4 choices (double-buffered slices fit 48 KiB)
+    constexpr int CR = (C >= 2 && C <= 4) ? C : 2;
+    if (OP == OP_INSERT && C == CR && relaxed_pipe_enabled()) {
+        const void *fr = (const void *)relaxed512_kernel<CR>;
+        unsigned grid = grid_for(fr, kTPB, 0, (n + kTPB - 1) / kTPB);
+        if (p.max_ctas && grid > p.max_ctas) grid = p.max_ctas;
+        return launch_words(relaxed512_kernel<CR>, grid, p, words, s, p, words, keys, n);
     }
     const void *fn = (const void *)blocks512_kernel<OP, C>;
     unsigned grid = grid_for(fn, kTPB, 0, (n + kTPB - 1) / kTPB);
