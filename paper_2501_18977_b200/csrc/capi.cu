@@ -668,9 +668,11 @@ static int host_pipeline(bc_filter *f, u64 *words, const u64 *h_keys, u64 n, int
     } pend[2];
     int rc = BC_OK;
     u64 chunk_i = 0;
-    for (u64 off = 0; off < n && rc == BC_OK; off += kStageKeys, ++chunk_i) {
+    // at least four chunks for mid-size batches, so copies overlap kernels
+    const u64 chunk = std::min(kStageKeys, std::max<u64>(1ull << 18, (n + 3) / 4));
+    for (u64 off = 0; off < n && rc == BC_OK; off += chunk, ++chunk_i) {
         const int b = (int)(chunk_i & 1);
-        const u64 len = std::min(kStageKeys, n - off);
+        const u64 len = std::min(chunk, n - off);
         CUDA_TRY(cudaEventSynchronize(st->done[b]));  // buffer b is free again
         if (pend[b].live && h_out && !out_pinned)
             std::memcpy(h_out + pend[b].off, st->h_out[b], pend[b].len);
