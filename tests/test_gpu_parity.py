@@ -407,3 +407,58 @@ def test_partitioned_single_choice_insert_bit_identical(golden, tmp_path):
     assert out.returncode == 0, out.stderr
     assert out.stdout.strip().splitlines()[-1] == case["words_sha256"]
 
+
+
+def _run_with_env(script, **env):
+    import subprocess
+    import sys
+
+    out = subprocess.run([sys.executable, "-c", script], env=dict(os.environ, **env),
+                         capture_output=True, text=True,
+                         cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    assert out.returncode == 0, out.stderr
+    return out.stdout.strip().splitlines()[-1]
+
+
+@pytest.mark.parametrize("persist", ["0", "1"])
+def test_l2_window_does_not_change_results(golden, persist):
+    """Filters launched with or without the L2-persisting window (BC_L2_PERSIST,
+    read at load, hence the subprocess) give the reference's bits and answers;
+    bc_l2_release between calls is harmless."""
+    meta, _ = golden
+    case = meta["cfg2_small"]
+    script = (
+        "import hashlib, numpy as np, torch, paper_2501_18977_b200 as bb\n"
+        "from paper_2501_18977_b200 import _native\n"
+        f"cfg = bb.FilterConfig(**{dict(case['config'])!r})\n"
+        "f = bb.Filter.from_config(cfg)\n"
+        f"keys = bb.even_keys({case['n_insert']}, {case['insert_seed']})\n"
+        "f.insert_many(torch.from_numpy(keys).cuda())\n"
+        "_native.lib().bc_l2_release()\n"
+        f"probes = np.concatenate([keys[:max(1, {case['n_insert']} // 2)], "
+        f"bb.odd_keys({case['n_neg']}, {case['neg_seed']})])\n"
+        "out = f.contains_many(torch.from_numpy(probes).cuda()).cpu().numpy().astype(np.uint8)\n"
+        "print(hashlib.sha256(f.storage.words.tobytes()).hexdigest(), "
+        "hashlib.sha256(out.tobytes()).hexdigest())\n")
+    words, answers = _run_with_env(script, BC_L2_PERSIST=persist).split()
+    assert words == case["words_sha256"]
+    assert answers == case["out_sha256"]
+
+
+def test_unpipelined_relaxed_insert_within_tolerance(golden):
+    """BC_RELAXED_PIPE=0 (the plain two-phase tile) meets the same relaxed
+    tolerances as the default pipelined kernel."""
+    meta, _ = golden
+    case = meta["bc3_k12_20k"]
+    script = (
+        "import numpy as np, torch, paper_2501_18977_b200 as bb\n"
+        "from paper_2501_18977_b200.filters import CostModel\n"
+        f"cfg = bb.FilterConfig(**{dict(case['config'])!r})\n"
+        "f = bb.Filter.from_config(cfg, insert_mode='relaxed')\n"
+        f"keys = bb.even_keys({case['n_insert']}, {case['insert_seed']})\n"
+        "f.insert_many(keys)\n"
+        "assert f.contains_many(keys).all()\n"
+        f"print(f.count_hits(bb.odd_keys({case['n_neg']}, {case['neg_seed']})))\n")
+    hits = int(_run_with_env(script, BC_RELAXED_PIPE="0"))
+    ref = case["hits_neg"]
+    assert abs(hits - ref) <= 0.1 * ref + 3 * np.sqrt(2.0 * max(ref, 1)) + 1
