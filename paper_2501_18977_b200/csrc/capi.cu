@@ -255,10 +255,11 @@ static int ensure_ordered_scratch(bc_filter *f, cudaStream_t s) {
     if (f->d_owner) return BC_OK;
     const u64 M = f->kp.num_blocks;
     // Chunk size trades claim rounds (grid syncs) against conflicts (visits per
-    // key).  Measured on B200 (bench.py --insert-mode ordered): cfg1 (M = 2^15)
-    // is best at chunk = M (182 Mkeys/s vs 96 at M/8), cfg3 (M = 2^23) at
-    // M/16 = 2^19 (1261 vs 1125 at M/8), i.e. about two keys per resident thread.
-    u64 chunk = std::min<u64>(M, 1ull << 19);
+    // key).  Measured on B200 (bench.py --insert-mode ordered, warp-aggregated
+    // pending-list appends): cfg1 (M = 2^15) is best at 2M (309 Mkeys/s vs 268
+    // at M, 150 at M/4); cfg3 (M = 2^23) at 2^21..2^22 (1795 vs 1467 at 2^19,
+    // 740 at 2^24).
+    u64 chunk = std::min<u64>(2 * M, 1ull << 22);
     if (const char *e = std::getenv("BC_ORDERED_CHUNK")) chunk = std::strtoull(e, nullptr, 10);
     chunk = std::max<u64>(chunk, 256);
     chunk = std::min<u64>(chunk, 1ull << 24);

@@ -301,8 +301,17 @@ __global__ void __launch_bounds__(256) ordered_kernel(const __grid_constant__ KP
                 } else if (win) {
                     build_mask_generic(p, x, mask);
                     insert_generic(p, words, x, mask);
-                } else {
-                    nxt[atomicAdd(cnt, 1u)] = li;
+                }
+                // losers go to the next pending list: one counter atomic per
+                // warp (list order is irrelevant, priority is the key index)
+                const u32 am = __activemask();
+                const u32 lm = __ballot_sync(am, !win);
+                if (lm) {
+                    const int lane = threadIdx.x & 31, leader = __ffs(lm) - 1;
+                    u32 base = 0;
+                    if (lane == leader) base = atomicAdd(cnt, (u32)__popc(lm));
+                    base = __shfl_sync(am, base, leader);
+                    if (!win) nxt[base + __popc(lm & ((1u << lane) - 1u))] = li;
                 }
             }
             grid.sync();

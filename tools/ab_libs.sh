@@ -7,5 +7,5 @@ cd "${GRAFT_REPO_ROOT:-$(dirname "$0")/..}"
 for c in ${CFGS:-2}; do for rep in $(seq ${REPS:-1}); do for lib in ${LIBS:-""}; do
   [ "$lib" = "cur" ] && lib=""
   L=paper_2501_18977_b200/libbbchoc${lib:+_$lib}.so
-  BC_LIBRARY=$PWD/$L timeout 600 python bench.py --config $c --no-e2e --no-cpu-baseline --steps ${STEPS:-20} 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read().strip().splitlines()[-1]); print($c, '${lib:-cur}', d['value'], d['insert_mkeys_s'], d['lookup_mkeys_s'], d['fpr'], d['false_negatives'])"
+  BC_LIBRARY=$PWD/$L timeout 600 python bench.py --config $c --no-e2e --no-cpu-baseline --steps ${STEPS:-20} ${EXTRA:-} 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read().strip().splitlines()[-1]); print($c, '${lib:-cur}', d['value'], d['insert_mkeys_s'], d['lookup_mkeys_s'], d['fpr'], d['false_negatives'])"
 done; done; done
