@@ -16,9 +16,11 @@ inputs resident in HBM.  ``e2e``: the same metric through the public API
 included.  ``--impl reference`` times the CPU oracle (a C restatement of the
 reference's numba kernels, oracle/) on all host cores instead.
 
-Multi-GPU (torchrun, one rank per GPU, NCCL): rank 0 builds (T = 1, so the
-reference layout has no subfilters), the words are NCCL-broadcast, and every
-rank answers its own lookup batch (weak scaling); value = all keys / max
+Multi-GPU (torchrun, one rank per GPU, NCCL): every rank answers its own
+lookup batch (weak scaling); the build is shared for order-free kinds (c = 1,
+standard: each rank ORs a slice of the keys into its replica, then the
+replicas are OR-all-reduced) and done on rank 0 + NCCL-broadcast for c >= 2
+(T = 1, so the reference layout has no subfilters).  value = all keys / max
 rank time.
 """
 
@@ -395,6 +397,7 @@ def run_ours(args, cfg):
 
     import paper_2501_18977_b200 as bb
     from paper_2501_18977_b200 import _native
+    from paper_2501_18977_b200 import distributed as D
 
     world, rank, local = dist_env()
     if DIST:
@@ -411,15 +414,22 @@ def run_ours(args, cfg):
     out = torch.empty(queries.numel(), dtype=torch.uint8, device=dev)
     words = filt.storage.d_words
     stream = torch.cuda.current_stream()
-    builder = rank == 0
+    # N > 1: order-free kinds (c = 1, standard) build from per-rank key slices
+    # and OR-all-reduce the replicas; c >= 2 builds on rank 0 and broadcasts
+    split = DIST and world > 1 and D.order_free(filt)
+    builder = split or rank == 0
+    lo, hi = D.slice_bounds(cfg["n"], world)[rank] if split else (0, cfg["n"])
+    my_keys = keys[lo:hi]
 
     def step(ev):
         ev[0].record(stream)
         if builder:
             words.zero_()
-            filt.insert_many(keys)
+            filt.insert_many(my_keys)
         ev[1].record(stream)
-        if DIST:
+        if split:
+            D.or_allreduce_(words.view(torch.int64))
+        elif DIST:
             dist.broadcast(words.view(torch.int64), src=0)
         ev[2].record(stream)
         filt.contains_many(queries, out=out)
@@ -477,10 +487,10 @@ def run_ours(args, cfg):
     l0 = _native.launch_count()
     if builder:
         words.zero_()
-        filt.insert_many(keys)
+        filt.insert_many(my_keys)
     torch.cuda.synchronize()
     launches_ins = max(1, _native.launch_count() - l0)
-    ins_bytes = insert_bytes(cfg["c"]) * cfg["n"]
+    ins_bytes = insert_bytes(cfg["c"]) * (hi - lo)
     look_bytes = cfg["lookup_bytes"] * cfg["nq"]
     if look_ms >= ins_ms:
         kname, kms, kbytes, klaunch = "contains", look_ms, look_bytes, 1
@@ -510,12 +520,16 @@ def run_ours(args, cfg):
                  "synthetic: reference key streams even_keys(n, 11) / odd_keys(., 12) "
                  "generated on the device (bit-identical to numpy), seeded 50/50 mix"),
         "config": {"workload": cfg["workload"], "insert_mode": mode,
-                   "parallelism": f"build on rank 0 + NCCL broadcast, lookups dp{world}",
+                   "parallelism": (f"build from per-rank key slices + OR all-reduce "
+                                   f"(all-to-all, OR fold, all-gather), lookups dp{world}"
+                                   if split else
+                                   f"build on rank 0 + NCCL broadcast, lookups dp{world}"),
                    "l2": "inputs larger than L2 (keys re-read every step); filter words "
                          "L2-persisting when the filter fits L2 (BC_L2_PERSIST)"},
         "insert_mkeys_s": round(cfg["n"] / ins_ms / 1e3, 2) if builder else None,
         "lookup_mkeys_s": round(cfg["nq"] / look_ms / 1e3, 2),
         "broadcast_ms": round(bc_ms, 3) if DIST else None,
+        "replication": ("or_allreduce" if split else "broadcast") if DIST else None,
         "false_negatives": fn, "fpr": fp / max(n_neg, 1),
         "gpu_launches": int(launches),
         "clocks": clocks,
@@ -548,14 +562,21 @@ def run_e2e(args, cfg, filt, keys, queries, world, rank, dev):
     h_q.copy_(queries.cpu())
     h_out = torch.empty(queries.numel(), dtype=torch.uint8, pin_memory=True)
     nk, nq, no = h_keys.numpy(), h_q.numpy(), h_out.numpy()
-    builder = rank == 0
+    from paper_2501_18977_b200 import distributed as D
+
+    split = DIST and world > 1 and D.order_free(filt)
+    builder = split or rank == 0
+    lo, hi = D.slice_bounds(cfg["n"], world)[rank] if split else (0, cfg["n"])
+    nk_mine = nk[lo:hi]
     words = filt.storage.d_words
 
     def step():
         if builder:
             words.zero_()
-            filt.insert_many(nk)                 # H2D of the keys inside the call
-        if DIST:
+            filt.insert_many(nk_mine)            # H2D of the keys inside the call
+        if split:
+            D.or_allreduce_(words.view(torch.int64))
+        elif DIST:
             dist.broadcast(words.view(torch.int64), src=0)
         filt.contains_many(nq, out=no)           # H2D queries, D2H answers
 
@@ -582,7 +603,7 @@ def run_e2e(args, cfg, filt, keys, queries, world, rank, dev):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         el = float(t.item())
     keys_per_step = cfg["n"] + world * cfg["nq"]
-    h2d = int(8 * ((cfg["n"] if builder else 0) + cfg["nq"]))
+    h2d = int(8 * ((hi - lo if builder else 0) + cfg["nq"]))
     d2h = int(cfg["nq"])
     return {"value": round(keys_per_step * steps / el / 1e6, 2), "unit": "Mkeys/s",
             "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,

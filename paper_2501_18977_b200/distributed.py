@@ -10,15 +10,20 @@ Two data-parallel patterns, both from the reference's own parallel design
   all-reduced).  The lookup itself has no communication, so it scales with
   the number of GPUs; the one-time broadcast is reported separately.
 
-* **Inserts go to hash-partitioned subfilters only where the reference's
-  layout has them** (``shards = T > 1``).  Shard s owns words
+* **Order-free builds (one choice, standard) split the keys.**  Each rank
+  ORs a contiguous slice of the stream into its replica, then the replicas
+  are OR-all-reduced (``or_allreduce_words``); the result is the sequential
+  bit array because OR commutes.
+
+* **Multi-choice inserts go to hash-partitioned subfilters only where the
+  reference's layout has them** (``shards = T > 1``).  Shard s owns words
   [s*wps, (s+1)*wps); rank r owns the contiguous shard range
   [r*T/W, (r+1)*T/W).  Keys are routed with the shard hash h0 on the
   device; each rank inserts, in stream order, the keys of its shards only
   (so ordered builds stay bit-identical to the reference's sequential
   build, sharding.py:1-9), then an all-gather of the W contiguous word
-  ranges replicates the filter.  With T = 1 (every BASELINE config) rank 0
-  builds and broadcasts.
+  ranges replicates the filter.  With T = 1 and c >= 2 rank 0 builds and
+  broadcasts.
 
 Every collective acts on the filter's word tensor; no collective runs inside
 a lookup or insert kernel.  The functions only use the filter's public
@@ -145,13 +150,70 @@ def gather_subfilters(filt, group=None) -> None:
     filt.storage.device_modified()
 
 
+def or_allreduce_(words: torch.Tensor, group=None) -> torch.Tensor:
+    """In-place bitwise-OR all-reduce of an int64 word tensor (NCCL has no OR
+    reduction): an all-to-all of W equal word ranges (the reduce-scatter
+    layout), an OR fold of the W pieces each rank received, and an all-gather
+    of the folded ranges.  Every rank moves 2 (W-1)/W of the array, like a
+    ring all-reduce.  Stream-ordered, no host synchronisation."""
+    rank, world = _rank_world(group)
+    if world == 1:
+        return words
+    n = words.numel()
+    span = -(-n // world)
+    pad = span * world - n
+    src = words if pad == 0 else torch.cat([words, words.new_zeros(pad)])
+    recv = torch.empty_like(src)
+    dist.all_to_all_single(recv, src, group=group)
+    pieces = recv.view(world, span)  # piece j: rank j's words of range `rank`
+    acc = pieces[0].clone()
+    for j in range(1, world):
+        acc.bitwise_or_(pieces[j])
+    if dist.get_backend(group) == "nccl":
+        dist.all_gather_into_tensor(src, acc, group=group)
+    else:
+        outs = [torch.empty_like(acc) for _ in range(world)]
+        dist.all_gather(outs, acc, group=group)
+        torch.cat(outs, out=src)
+    if pad:
+        words.copy_(src[:n])
+    return words
+
+
+def or_allreduce_words(filt, group=None) -> None:
+    """OR all-reduce of the ranks' bit arrays (or_allreduce_) and the sum of
+    their inserted-key counts."""
+    words = _words_i64(filt)
+    or_allreduce_(words, group=group)
+    counts = torch.tensor([filt.inserted], dtype=torch.int64, device=words.device)
+    dist.all_reduce(counts, group=group)
+    filt.inserted = int(counts.item())
+    filt.storage.device_modified()
+
+
+def order_free(filt) -> bool:
+    """Inserts commute (one choice, or the standard kind): the bit array is
+    the OR of the keys' masks whatever the order (_kernels.py:142-147,221)."""
+    return filt.kind in ("blocked", "standard")
+
+
 def build_subfilters(filt, keys, group=None, mode: str | None = None):
     """Insert a key stream (identical on every rank) into ``filt``.
 
     ``shards > 1``: each rank inserts the keys of its shard range (device
     routing, no data exchange), then the ranges are all-gathered.
-    ``shards == 1``: rank 0 inserts everything, then broadcasts."""
+    ``shards == 1``, order-free kinds: each rank inserts a contiguous slice
+    into its replica, then the replicas are OR-all-reduced.
+    ``shards == 1``, c >= 2: rank 0 inserts everything, then broadcasts."""
     rank, world = _rank_world(group)
+    if filt.shards == 1 and world > 1 and order_free(filt):
+        part, _, _ = _local_slice(keys, group)
+        before = filt.inserted
+        filt.insert_many(part, mode=mode) if mode else filt.insert_many(part)
+        filt.inserted -= before  # this rank's share; summed by the all-reduce
+        or_allreduce_words(filt, group=group)
+        filt.inserted += before
+        return filt
     if filt.shards == 1 or world == 1:
         if rank == 0:
             filt.insert_many(keys, mode=mode) if mode else filt.insert_many(keys)

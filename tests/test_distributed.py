@@ -38,6 +38,7 @@ class OracleFilter:
 
     def __init__(self, **kw):
         self.o = orc.make_filter(**kw)
+        self.kind = kw["kind"]
         self.shards = self.o.shards
         self.inserted = 0
         self.storage = SimpleNamespace(d_words=torch.from_numpy(self.o.words),
@@ -103,13 +104,29 @@ def _worker(rank, world, port, case):
             D.gather_subfilters(f)
             assert np.array_equal(f.o.words, ref.words)
             assert f.inserted == keys.shape[0]
+        elif case in ("or_blocked", "or_standard"):
+            kind = case[3:]
+            cfg = dict(kind=kind, k=9, n_capacity=30_001, seed=23,
+                       **({"block_bits": 512} if kind == "blocked" else {}))
+            ref2 = orc.make_filter(**cfg)
+            ref2.insert_many(keys)
+            f = OracleFilter(**cfg)
+            D.build_subfilters(f, keys)
+            assert np.array_equal(f.o.words, ref2.words)
+            assert f.inserted == keys.shape[0]
     finally:
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("case", ["subfilters", "broadcast", "lookups", "exchange"])
+@pytest.mark.parametrize("case", ["subfilters", "broadcast", "lookups", "exchange",
+                                  "or_blocked", "or_standard"])
 def test_two_rank_gloo(case):
     mp.spawn(_worker, args=(2, free_port(), case), nprocs=2, join=True)
+
+
+def test_three_rank_or_build_with_padding():
+    """OR all-reduce when the word count does not split evenly over ranks."""
+    mp.spawn(_worker, args=(3, free_port(), "or_blocked"), nprocs=3, join=True)
 
 
 def test_slice_bounds_cover():
@@ -149,6 +166,14 @@ def _nccl_worker(rank, world, port):
         probes = np.concatenate([keys[:5000], orc.odd_keys(7001, 9)])
         assert np.array_equal(D.contains_many_sharded(f, probes), ref.contains_many(probes))
         assert D.count_hits_sharded(f, probes) == int(ref.contains_many(probes).sum())
+        # order-free build from key slices + OR all-reduce
+        g = bb.Filter.from_config(bb.FilterConfig(kind="blocked", k=9, n_capacity=30_001,
+                                                  seed=23))
+        D.build_subfilters(g, torch.from_numpy(keys).cuda())
+        ref2 = orc.make_filter(kind="blocked", k=9, n_capacity=30_001, seed=23)
+        ref2.insert_many(keys)
+        assert np.array_equal(g.storage.words, ref2.words)
+        assert g.inserted == keys.shape[0]
     finally:
         dist.destroy_process_group()
 
