@@ -254,19 +254,22 @@ static int check_device(bc_filter *f) {
 static int ensure_ordered_scratch(bc_filter *f, cudaStream_t s) {
     if (f->d_owner) return BC_OK;
     const u64 M = f->kp.num_blocks;
-    // Chunk size trades claim rounds (grid syncs) against conflicts (visits per
-    // key).  Measured on B200 (bench.py --insert-mode ordered, warp-aggregated
-    // pending-list appends): cfg1 (M = 2^15) is best at 2M (309 Mkeys/s vs 268
-    // at M, 150 at M/4); cfg3 (M = 2^23) at 2^21..2^22 (1795 vs 1467 at 2^19,
-    // 740 at 2^24).
-    u64 chunk = std::min<u64>(2 * M, 1ull << 22);
+    // Window (pending keys per round) trades rounds (grid syncs) against
+    // conflicts (claims per committed key).  Measured on B200 with the
+    // sliding-window kernel (bench.py --insert-mode ordered): cfg1 (M = 2^15)
+    // is best at M/2 (550 Mkeys/s vs 515 at 2M, 440 at M/4); cfg3 (M = 2^23)
+    // at 2^19 (1765 vs 1602 at 2^20, 442 at 2^22); cfg5 (M = 2^27) 1781 at
+    // 2^18, 1896 at 2^20.
+    u64 chunk = std::min<u64>(M / 2, 1ull << 19);
     if (const char *e = std::getenv("BC_ORDERED_CHUNK")) chunk = std::strtoull(e, nullptr, 10);
     chunk = std::max<u64>(chunk, 256);
     chunk = std::min<u64>(chunk, 1ull << 24);
-    CUDA_TRY(cudaMalloc(&f->d_owner, sizeof(u64) * M));
+    // two claim arrays: the sliding-window kernel claims for round r + 1
+    // while round r's claims are being checked
+    CUDA_TRY(cudaMalloc(&f->d_owner, sizeof(u64) * 2 * M));
     CUDA_TRY(cudaMalloc(&f->d_lists, sizeof(u32) * 2 * chunk));
     CUDA_TRY(cudaMalloc(&f->d_state, sizeof(u32) * 4));
-    CUDA_TRY(cudaMemsetAsync(f->d_owner, 0xff, sizeof(u64) * M, s));
+    CUDA_TRY(cudaMemsetAsync(f->d_owner, 0xff, sizeof(u64) * 2 * M, s));
     CUDA_TRY(cudaMemsetAsync(f->d_state, 0, sizeof(u32) * 4, s));
     f->chunk = chunk;
     f->rounds_bound = 0;
@@ -328,7 +331,7 @@ static int insert_device(bc_filter *f, u64 *words, const u64 *keys, u64 n, int m
     // every round commits at least one key, so rounds <= keys: re-arm the
     // round tags long before the 32-bit counter could wrap
     if (f->rounds_bound + n >= (1ull << 31)) {
-        CUDA_TRY(cudaMemsetAsync(f->d_owner, 0xff, sizeof(u64) * f->kp.num_blocks, s));
+        CUDA_TRY(cudaMemsetAsync(f->d_owner, 0xff, sizeof(u64) * 2 * f->kp.num_blocks, s));
         CUDA_TRY(cudaMemsetAsync(f->d_state, 0, sizeof(u32) * 4, s));
         f->rounds_bound = 0;
     }

@@ -326,6 +326,91 @@ __global__ void __launch_bounds__(256) ordered_kernel(const __grid_constant__ KP
     if (gtid == 0) state[0] = round;
 }
 
+// Exact stream order, sliding window.  Same commit rule as ordered_kernel (a
+// pending key commits iff its claim is the minimum on every candidate), but:
+//  * one pass and one grid sync per round: a key checks the claims made in
+//    the previous round (owner[round & 1]), and if it loses it immediately
+//    claims for the next round in the other owner array;
+//  * instead of fixed chunks, a window of up to `window` pending keys is
+//    refilled every round with the next keys of the stream, so rounds never
+//    run near-empty at the tail of a chunk.
+// Keys enter in index order, so every earlier key that shares a block with a
+// pending key is either committed or pending (and then wins that block):
+// the result is the sequential one.  Claims carry (~round) in the high word,
+// so stale values of older rounds (and launches) always lose.  state[0] is
+// the round counter; state[1..3] are rotating append counters (round r
+// appends to counter r % 3 and zeroes counter (r + 1) % 3, last read two
+// syncs ago).
+__global__ void __launch_bounds__(256) ordered_window_kernel(
+    const __grid_constant__ KParams p, u64 *__restrict__ words, const u64 *__restrict__ keys,
+    u64 n, u64 window, u64 *__restrict__ owner, u32 *__restrict__ lists,
+    u32 *__restrict__ state) {
+    cg::grid_group grid = cg::this_grid();
+    const u64 gtid = blockIdx.x * (u64)blockDim.x + threadIdx.x;
+    const u64 gstride = (u64)gridDim.x * blockDim.x;
+    const int lane = threadIdx.x & 31;
+    __shared__ u32 ocol[8][16][32];  // fast path: per-thread mask columns
+    u32 *col = &ocol[threadIdx.x >> 5][0][threadIdx.x & 31];
+    const bool fast = p.fast_random && p.wpb == 8;
+    const u64 M = p.num_blocks;
+    u32 round = __ldcg(state);
+    u32 *cur = lists, *nxt = lists + window;
+    u64 npend = 0, next = 0;
+    u64 mask[kMaxWpb];
+    while (npend > 0 || next < n) {
+        const u64 admit = min(window - npend, n - next);
+        const u64 *own_cur = owner + (round & 1u) * M;
+        u64 *own_nxt = owner + ((round + 1u) & 1u) * M;
+        const u64 claim_cur = (u64)(0xffffffffu - round) << 32;
+        const u64 claim_nxt = (u64)(0xffffffffu - (round + 1u)) << 32;
+        u32 *cnt = state + 1 + round % 3u;
+        if (gtid == 0) state[1 + (round + 1u) % 3u] = 0;
+        for (u64 t = gtid; t < npend + admit; t += gstride) {
+            u32 li;
+            bool lose = true;
+            if (t < npend) {
+                li = __ldcg(cur + t);
+                const u64 x = keys[li];
+                bool win = true;
+                for (u32 ci = 0; ci < p.c; ++ci)
+                    win &= __ldcg(own_cur + block_index(p, x, ci)) == (claim_cur | li);
+                if (win && fast) {
+                    insert_fast512(p, words, x, col);
+                } else if (win) {
+                    build_mask_generic(p, x, mask);
+                    insert_generic(p, words, x, mask);
+                }
+                lose = !win;
+            } else {
+                li = (u32)(next + (t - npend));  // newly admitted
+            }
+            if (lose) {
+                const u64 x = keys[li];
+                for (u32 ci = 0; ci < p.c; ++ci)
+                    atomicMin((unsigned long long *)(own_nxt + block_index(p, x, ci)),
+                              (unsigned long long)(claim_nxt | li));
+            }
+            const u32 am = __activemask();
+            const u32 lm = __ballot_sync(am, lose);
+            if (lm) {
+                const int leader = __ffs(lm) - 1;
+                u32 base = 0;
+                if (lane == leader) base = atomicAdd(cnt, (u32)__popc(lm));
+                base = __shfl_sync(am, base, leader);
+                if (lose) nxt[base + __popc(lm & ((1u << lane) - 1u))] = li;
+            }
+        }
+        grid.sync();
+        npend = __ldcg(cnt);
+        next += admit;
+        u32 *tmp = cur;
+        cur = nxt;
+        nxt = tmp;
+        ++round;
+    }
+    if (gtid == 0) state[0] = round;
+}
+
 template <int OP>
 __global__ void __launch_bounds__(256) flat_kernel(const __grid_constant__ KParams p,
                                                    u64 *__restrict__ words,
@@ -654,10 +739,32 @@ cudaError_t launch_blocks(int op, const KParams &p, u64 *words, const u64 *keys,
     return cudaGetLastError();
 }
 
+static bool ordered_window_enabled() {  // BC_ORDERED_WINDOW=0: fixed chunks
+    static const bool on = [] {
+        const char *e = getenv("BC_ORDERED_WINDOW");
+        return e == nullptr || atoi(e) != 0;
+    }();
+    return on;
+}
+
 cudaError_t launch_ordered(const KParams &p, u64 *words, const u64 *keys, u64 n, u64 chunk,
                            u64 *owner, u32 *lists, u32 *state, cudaStream_t s) {
     if (n == 0) return cudaSuccess;
     l2_release();
+    if (ordered_window_enabled()) {
+        // owner holds two arrays of num_blocks claims; the append counters
+        // state[1..3] start at zero, the round counter state[0] carries over
+        cudaError_t e = cudaMemsetAsync(state + 1, 0, 3 * sizeof(u32), s);
+        if (e != cudaSuccess) return e;
+        const void *fw = (const void *)ordered_window_kernel;
+        const unsigned grid = grid_for(fw, 256, 0, (chunk + 255) / 256);
+        KParams pp = p;
+        void *args[] = {(void *)&pp, (void *)&words, (void *)&keys, (void *)&n,
+                        (void *)&chunk, (void *)&owner, (void *)&lists, (void *)&state};
+        e = cudaLaunchCooperativeKernel(fw, dim3(grid), dim3(256), args, 0, s);
+        count_launch();
+        return e;
+    }
     const void *fn = (const void *)ordered_kernel;
     const unsigned grid = grid_for(fn, 256, 0, (chunk + 255) / 256);
     KParams pp = p;
