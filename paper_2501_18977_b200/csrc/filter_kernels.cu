@@ -4,8 +4,13 @@
 //                            blocks, two-phase tile (blocks.cuh)
 //   generic_kernel<OP>       thread per key, any block width (toy 8/16/32,
 //                            64..4096 bits)
-//   ordered_kernel           exact stream-order insert for c >= 2: claim
-//                            rounds inside one cooperative launch
+//   relaxed512_kernel<C>     relaxed (atomic) multi-choice inserts, next
+//                            tile's hashing overlapped with the loads
+//   lookup512_kernel<C, K>   lookups: staged blocks, early exit over choices
+//   lookup512_pipe_kernel<K> single-choice lookups, two tiles in flight
+//   ordered_window_kernel    exact stream-order insert for c >= 2: claim
+//                            rounds over a sliding window, one cooperative
+//                            launch (ordered_kernel: fixed-chunk variant)
 //   flat_kernel<OP>          standard Bloom filter (k global bits)
 //   hist512_kernel / hist_generic_kernel   per-block popcount tally
 //   eval_hash_kernel         one hash over a key array (routing)
