@@ -462,3 +462,19 @@ def test_unpipelined_relaxed_insert_within_tolerance(golden):
     hits = int(_run_with_env(script, BC_RELAXED_PIPE="0"))
     ref = case["hits_neg"]
     assert abs(hits - ref) <= 0.1 * ref + 3 * np.sqrt(2.0 * max(ref, 1)) + 1
+
+
+@pytest.mark.parametrize("name", ["cfg1", "bc3_k12_20k", "bc2_k6_t4", "bc8_k5"])
+def test_ordered_build_in_several_calls(golden, name):
+    """Exact-order inserts split over several calls (ragged sizes, the claim
+    state carried between launches) give the reference's bit array."""
+    meta, _ = golden
+    case = meta[name]
+    f = bb.Filter.from_config(config_of(case))
+    keys, _ = probes_of(case)
+    n = keys.shape[0]
+    cuts = [0, 1, 257, n // 3, n // 3 + 1, (2 * n) // 3, n]
+    for a, b in zip(cuts[:-1], cuts[1:]):
+        f.insert_many(keys[a:b])
+    assert sha(f.storage.words) == case["words_sha256"]
+    assert f.inserted == n
