@@ -478,3 +478,29 @@ def test_ordered_build_in_several_calls(golden, name):
         f.insert_many(keys[a:b])
     assert sha(f.storage.words) == case["words_sha256"]
     assert f.inserted == n
+
+
+@pytest.mark.parametrize("kind,c,strategy,bb_bits", [
+    ("standard", None, "random", 512), ("blocked", 1, "random", 512),
+    ("blowchoc", 2, "random", 512), ("blowchoc", 3, "distinct", 512),
+    ("blowchoc", 2, "random", 128), ("blocked", 1, "random", 16),
+])
+def test_extreme_keys(kind, c, strategy, bb_bits):
+    """Edge keys (0, 1, 2^32 +- 1, 2^63, 2^64 - 1, all-ones halves) and their
+    neighbours inserted and looked up: bits and answers equal the oracle's."""
+    edge = [0, 1, 2, 2**32 - 1, 2**32, 2**32 + 1, 2**63 - 1, 2**63, 2**63 + 1,
+            2**64 - 2, 2**64 - 1, 0xFFFFFFFF00000000, 0x00000000FFFFFFFF,
+            0x5555555555555555, 0xAAAAAAAAAAAAAAAA]
+    keys = np.array(edge, dtype=np.uint64)
+    kw = dict(kind=kind, k=7, size_bits=4096, seed=99, strategy=strategy,
+              block_bits=bb_bits)
+    if c is not None:
+        kw["choices"] = c
+    o = orc.make_filter(kind, k=7, choices=c, strategy=strategy, block_bits=bb_bits,
+                        size_bits=4096, seed=99)
+    o.insert_many(keys[::2])
+    f = bb.Filter.from_config(bb.FilterConfig(**kw))
+    f.insert_many(keys[::2])
+    np.testing.assert_array_equal(f.storage.words, o.words)
+    np.testing.assert_array_equal(f.contains_many(keys), o.contains_many(keys))
+    assert f.contains_many(keys[::2]).all()
