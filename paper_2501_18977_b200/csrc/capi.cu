@@ -87,6 +87,8 @@ struct bc_filter {
     u32 *d_lists = nullptr;
     u32 *d_state = nullptr;
     u64 chunk = 0;
+    u64 slots = 0;        // claim slots per owner array
+    u64 owner_words = 0;  // allocated u64 claim tags
     u64 rounds_bound = 0;
 };
 
@@ -264,14 +266,32 @@ static int ensure_ordered_scratch(bc_filter *f, cudaStream_t s) {
     if (const char *e = std::getenv("BC_ORDERED_CHUNK")) chunk = std::strtoull(e, nullptr, 10);
     chunk = std::max<u64>(chunk, 256);
     chunk = std::min<u64>(chunk, 1ull << 24);
+    // Claim slots: one per block up to 2^24 blocks, else 2^24 slots with the
+    // blocks hashed onto them (spurious conflicts only delay commits).
+    // Measured (bench.py --insert-mode ordered): cfg5 (M = 2^27) 1966 ->
+    // 2095 Mkeys/s with 2^24 hashed slots, and 2 GB -> 256 MB of claim tags;
+    // cfg3 (M = 2^23) loses with fewer slots than blocks (1550 at 2^22, 1098
+    // at 2^20 vs 1761).  BC_ORDERED_SLOTS overrides (0 = one per block).
+    u64 slots = M;
+    u64 want = 1ull << 24;
+    if (const char *e = std::getenv("BC_ORDERED_SLOTS")) want = std::strtoull(e, nullptr, 10);
+    if (want) {
+        u64 pow2 = 1;
+        while (pow2 < want) pow2 <<= 1;
+        if (pow2 < M) slots = pow2;
+    }
     // two claim arrays: the sliding-window kernel claims for round r + 1
-    // while round r's claims are being checked
-    CUDA_TRY(cudaMalloc(&f->d_owner, sizeof(u64) * 2 * M));
+    // while round r's claims are being checked (the fixed-chunk kernel,
+    // BC_ORDERED_WINDOW=0, uses one array of M)
+    const u64 owner_words = std::max<u64>(2 * slots, M);
+    CUDA_TRY(cudaMalloc(&f->d_owner, sizeof(u64) * owner_words));
     CUDA_TRY(cudaMalloc(&f->d_lists, sizeof(u32) * 2 * chunk));
     CUDA_TRY(cudaMalloc(&f->d_state, sizeof(u32) * 4));
-    CUDA_TRY(cudaMemsetAsync(f->d_owner, 0xff, sizeof(u64) * 2 * M, s));
+    CUDA_TRY(cudaMemsetAsync(f->d_owner, 0xff, sizeof(u64) * owner_words, s));
     CUDA_TRY(cudaMemsetAsync(f->d_state, 0, sizeof(u32) * 4, s));
     f->chunk = chunk;
+    f->slots = slots;
+    f->owner_words = owner_words;
     f->rounds_bound = 0;
     return BC_OK;
 }
@@ -331,14 +351,14 @@ static int insert_device(bc_filter *f, u64 *words, const u64 *keys, u64 n, int m
     // every round commits at least one key, so rounds <= keys: re-arm the
     // round tags long before the 32-bit counter could wrap
     if (f->rounds_bound + n >= (1ull << 31)) {
-        CUDA_TRY(cudaMemsetAsync(f->d_owner, 0xff, sizeof(u64) * 2 * f->kp.num_blocks, s));
+        CUDA_TRY(cudaMemsetAsync(f->d_owner, 0xff, sizeof(u64) * f->owner_words, s));
         CUDA_TRY(cudaMemsetAsync(f->d_state, 0, sizeof(u32) * 4, s));
         f->rounds_bound = 0;
     }
     for (u64 off = 0; off < n; off += (1ull << 30)) {
         const u64 len = std::min<u64>(1ull << 30, n - off);
-        CUDA_TRY(launch_ordered(f->kp, words, keys + off, len, f->chunk, f->d_owner, f->d_lists,
-                                f->d_state, s));
+        CUDA_TRY(launch_ordered(f->kp, words, keys + off, len, f->chunk, f->d_owner, f->slots,
+                                f->d_lists, f->d_state, s));
         f->rounds_bound += len;
     }
     return BC_OK;

@@ -346,10 +346,20 @@ __global__ void __launch_bounds__(256) ordered_kernel(const __grid_constant__ KP
 // the round counter; state[1..3] are rotating append counters (round r
 // appends to counter r % 3 and zeroes counter (r + 1) % 3, last read two
 // syncs ago).
+// Claim slot of block b: the block itself (slot_shift == 0), or a
+// multiplicative hash into 2^(64 - slot_shift) slots.  Two blocks sharing a
+// slot only make their keys wait for each other (a spurious conflict); keys
+// that share a block always share its slot, so commits stay exact, and the
+// oldest pending key still wins every slot it claims.  Hashed slots keep the
+// claim arrays L2-sized for filters with many blocks.
+__device__ __forceinline__ u64 owner_slot(u64 b, u32 slot_shift) {
+    return slot_shift ? (b * 0x9E3779B97F4A7C15ull) >> slot_shift : b;
+}
+
 __global__ void __launch_bounds__(256) ordered_window_kernel(
     const __grid_constant__ KParams p, u64 *__restrict__ words, const u64 *__restrict__ keys,
-    u64 n, u64 window, u64 *__restrict__ owner, u32 *__restrict__ lists,
-    u32 *__restrict__ state) {
+    u64 n, u64 window, u64 *__restrict__ owner, u64 slots, u32 slot_shift,
+    u32 *__restrict__ lists, u32 *__restrict__ state) {
     cg::grid_group grid = cg::this_grid();
     const u64 gtid = blockIdx.x * (u64)blockDim.x + threadIdx.x;
     const u64 gstride = (u64)gridDim.x * blockDim.x;
@@ -357,15 +367,14 @@ __global__ void __launch_bounds__(256) ordered_window_kernel(
     __shared__ u32 ocol[8][16][32];  // fast path: per-thread mask columns
     u32 *col = &ocol[threadIdx.x >> 5][0][threadIdx.x & 31];
     const bool fast = p.fast_random && p.wpb == 8;
-    const u64 M = p.num_blocks;
     u32 round = __ldcg(state);
     u32 *cur = lists, *nxt = lists + window;
     u64 npend = 0, next = 0;
     u64 mask[kMaxWpb];
     while (npend > 0 || next < n) {
         const u64 admit = min(window - npend, n - next);
-        const u64 *own_cur = owner + (round & 1u) * M;
-        u64 *own_nxt = owner + ((round + 1u) & 1u) * M;
+        const u64 *own_cur = owner + (round & 1u) * slots;
+        u64 *own_nxt = owner + ((round + 1u) & 1u) * slots;
         const u64 claim_cur = (u64)(0xffffffffu - round) << 32;
         const u64 claim_nxt = (u64)(0xffffffffu - (round + 1u)) << 32;
         u32 *cnt = state + 1 + round % 3u;
@@ -378,7 +387,8 @@ __global__ void __launch_bounds__(256) ordered_window_kernel(
                 const u64 x = keys[li];
                 bool win = true;
                 for (u32 ci = 0; ci < p.c; ++ci)
-                    win &= __ldcg(own_cur + block_index(p, x, ci)) == (claim_cur | li);
+                    win &= __ldcg(own_cur + owner_slot(block_index(p, x, ci), slot_shift)) ==
+                           (claim_cur | li);
                 if (win && fast) {
                     insert_fast512(p, words, x, col);
                 } else if (win) {
@@ -392,7 +402,8 @@ __global__ void __launch_bounds__(256) ordered_window_kernel(
             if (lose) {
                 const u64 x = keys[li];
                 for (u32 ci = 0; ci < p.c; ++ci)
-                    atomicMin((unsigned long long *)(own_nxt + block_index(p, x, ci)),
+                    atomicMin((unsigned long long *)(own_nxt +
+                                                     owner_slot(block_index(p, x, ci), slot_shift)),
                               (unsigned long long)(claim_nxt | li));
             }
             const u32 am = __activemask();
@@ -753,7 +764,7 @@ static bool ordered_window_enabled() {  // BC_ORDERED_WINDOW=0: fixed chunks
 }
 
 cudaError_t launch_ordered(const KParams &p, u64 *words, const u64 *keys, u64 n, u64 chunk,
-                           u64 *owner, u32 *lists, u32 *state, cudaStream_t s) {
+                           u64 *owner, u64 slots, u32 *lists, u32 *state, cudaStream_t s) {
     if (n == 0) return cudaSuccess;
     l2_release();
     if (ordered_window_enabled()) {
@@ -764,8 +775,11 @@ cudaError_t launch_ordered(const KParams &p, u64 *words, const u64 *keys, u64 n,
         const void *fw = (const void *)ordered_window_kernel;
         const unsigned grid = grid_for(fw, 256, 0, (chunk + 255) / 256);
         KParams pp = p;
-        void *args[] = {(void *)&pp, (void *)&words, (void *)&keys, (void *)&n,
-                        (void *)&chunk, (void *)&owner, (void *)&lists, (void *)&state};
+        u32 slot_shift = 0;  // identity slots when there is one per block
+        if (slots < p.num_blocks) slot_shift = 64u - (u32)__builtin_ctzll(slots);
+        void *args[] = {(void *)&pp,    (void *)&words,      (void *)&keys,  (void *)&n,
+                        (void *)&chunk, (void *)&owner,      (void *)&slots, (void *)&slot_shift,
+                        (void *)&lists, (void *)&state};
         e = cudaLaunchCooperativeKernel(fw, dim3(grid), dim3(256), args, 0, s);
         count_launch();
         return e;

@@ -504,3 +504,20 @@ def test_extreme_keys(kind, c, strategy, bb_bits):
     np.testing.assert_array_equal(f.storage.words, o.words)
     np.testing.assert_array_equal(f.contains_many(keys), o.contains_many(keys))
     assert f.contains_many(keys[::2]).all()
+
+
+@pytest.mark.parametrize("slots", ["64", "4096"])
+def test_ordered_build_with_hashed_claim_slots(golden, slots):
+    """Exact-order inserts with the claim tags hashed onto few slots
+    (BC_ORDERED_SLOTS, read when the scratch is allocated): spurious
+    conflicts only delay commits, the bits stay the reference's."""
+    meta, _ = golden
+    case = meta["bc3_k12_20k"]
+    script = (
+        "import hashlib, numpy as np, paper_2501_18977_b200 as bb\n"
+        f"cfg = bb.FilterConfig(**{dict(case['config'])!r})\n"
+        "f = bb.Filter.from_config(cfg)\n"
+        f"keys = bb.even_keys({case['n_insert']}, {case['insert_seed']})\n"
+        "f.insert_many(keys[:7000]); f.insert_many(keys[7000:])\n"
+        "print(hashlib.sha256(f.storage.words.tobytes()).hexdigest())\n")
+    assert _run_with_env(script, BC_ORDERED_SLOTS=slots) == case["words_sha256"]
