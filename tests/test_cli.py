@@ -146,12 +146,24 @@ def test_build_query_hist_fpr_end_to_end(kind, c, threads, tmp_path):
     assert int(row["N"]) == neg.size
     assert int(row["W"]) == int(ref.contains_many(neg).sum())
 
-    if kind != "standard":
-        r = run_cli("hist", "--filter", out)
-        assert r.returncode == 0, r.stderr.decode()
-        lines = r.stdout.decode().strip().splitlines()
-        counts = np.array([int(x.split("\t")[1]) for x in lines[1:]])
-        np.testing.assert_array_equal(counts, ref.block_histogram())
+    r = run_cli("hist", "--filter", out)  # standard: block-aligned windows
+    assert r.returncode == 0, r.stderr.decode()
+    lines = r.stdout.decode().strip().splitlines()
+    counts = np.array([int(x.split("\t")[1]) for x in lines[1:]])
+    np.testing.assert_array_equal(counts, ref.block_histogram())
+
+    # fpr from generated negatives (the device odd-key stream): the count
+    # equals the oracle's on the same numpy stream
+    import paper_2501_18977_b200 as bb
+    r = run_cli("fpr", "--filter", out, "--negatives", 300000, "--neg-seed", 77)
+    assert r.returncode == 0, r.stderr.decode()
+    header, vals = r.stdout.decode().strip().splitlines()
+    row = dict(zip(header.split("\t"), vals.split("\t")))
+    neg = np.concatenate([bb.odd_keys(min(bb.DEFAULT_CHUNK, 300000 - a),
+                                      bb.derive_seed(77, i))
+                          for i, a in enumerate(range(0, 300000, bb.DEFAULT_CHUNK))])
+    assert int(row["N"]) == 300000
+    assert int(row["W"]) == int(ref.contains_many(neg).sum())
 
 
 @pytest.mark.gpu
