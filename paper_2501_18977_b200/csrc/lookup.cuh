@@ -14,6 +14,13 @@
 //      for keys still pending, so a positive costs the blocks up to its first
 //      passing choice -- the reference's early exit (E[P] blocks, SURVEY
 //      §8(d)) rather than all c.
+//
+// Staging uses cp.async (LDGSTS, .L2::64B: no 128-byte line fill for a
+// 64-byte block).  Bit tests take bit (hi >> 23) of the low product word as a
+// funnel-shift rotate of word hi >> 28; with k known at compile time
+// (K > 0) they are fully unrolled.  Single-choice lookups use PipeStage /
+// stage_blocks / test_staged instead: two tiles per warp in flight, the next
+// tile's cp.async group outstanding while the current one is tested.
 #pragma once
 
 #include "common.cuh"
