@@ -195,8 +195,8 @@ __device__ __forceinline__ void relaxed_commit(const KParams &p, u64 *words,
         if (!noop) {
             const uint4 m = sel4(M, (p0 + u - s) & 3);
             u64 *dst = words + (u64)ws.blk[best][4 * g + p0 + u] * 8 + 2 * s;
-            red_or(dst, (u64)m.x | ((u64)m.y << 32));
-            red_or(dst + 1, (u64)m.z | ((u64)m.w << 32));
+            red_or_all(dst, (u64)m.x | ((u64)m.y << 32));
+            red_or_all(dst + 1, (u64)m.z | ((u64)m.w << 32));
         }
     }
 }
@@ -366,7 +366,7 @@ __device__ __forceinline__ void insert_fast512(const KParams &p, u64 *words, u64
     }
     u64 *dst = words + block_index(p, x, best) * 8;
 #pragma unroll
-    for (int w = 0; w < 8; ++w) red_or(dst + w, (u64)m[2 * w] | ((u64)m[2 * w + 1] << 32));
+    for (int w = 0; w < 8; ++w) red_or_all(dst + w, (u64)m[2 * w] | ((u64)m[2 * w + 1] << 32));
 }
 
 // Reference insert decision for one key against L2-coherent block reads.

@@ -131,8 +131,19 @@ __device__ __forceinline__ uint4 ld_block_cg(const uint4 *p) {
     return r;
 }
 
+// OR a word into global memory (RED, no return value), skipping zero words:
+// those still cost L2 atomic throughput, which bounds the L2-resident
+// single-choice insert (cfg2: 67.5 Gkeys/s skipped vs 58 unconditional).
 __device__ __forceinline__ void red_or(u64 *p, u64 v) {
     if (v) atomicOr((unsigned long long *)p, (unsigned long long)v);
+}
+
+// Unconditional RED: where the L2 atomics are not the bound (multi-choice
+// inserts wait on DRAM and latency), the branch around each RED (BSSY /
+// predicate / branch / BSYNC) costs more than the zero words (cfg5 relaxed
+// inserts +10%, cfg3 +4%, cfg1 +5%).
+__device__ __forceinline__ void red_or_all(u64 *p, u64 v) {
+    atomicOr((unsigned long long *)p, (unsigned long long)v);
 }
 
 }  // namespace bc
