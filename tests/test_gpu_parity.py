@@ -521,3 +521,28 @@ def test_ordered_build_with_hashed_claim_slots(golden, slots):
         "f.insert_many(keys[:7000]); f.insert_many(keys[7000:])\n"
         "print(hashlib.sha256(f.storage.words.tobytes()).hexdigest())\n")
     assert _run_with_env(script, BC_ORDERED_SLOTS=slots) == case["words_sha256"]
+
+
+@pytest.mark.parametrize("name,env", [("cfg2_small", {"BC_LOOKUP_PIPE": "0"}),
+                                      ("bc3_k12_20k", {"BC_ORDERED_WINDOW": "0"}),
+                                      ("cfg1", {"BC_ORDERED_WINDOW": "0"})])
+def test_fallback_kernels_match_reference(golden, name, env):
+    """The non-default kernel variants kept behind switches (unpipelined
+    single-choice lookups, fixed-chunk exact inserts) still give the
+    reference's bits and answers."""
+    meta, _ = golden
+    case = meta[name]
+    script = (
+        "import hashlib, numpy as np, paper_2501_18977_b200 as bb\n"
+        f"cfg = bb.FilterConfig(**{dict(case['config'])!r})\n"
+        "f = bb.Filter.from_config(cfg)\n"
+        f"keys = bb.even_keys({case['n_insert']}, {case['insert_seed']})\n"
+        "f.insert_many(keys)\n"
+        f"probes = np.concatenate([keys[:max(1, {case['n_insert']} // 2)], "
+        f"bb.odd_keys({case['n_neg']}, {case['neg_seed']})])\n"
+        "out = f.contains_many(probes).astype(np.uint8)\n"
+        "print(hashlib.sha256(f.storage.words.tobytes()).hexdigest(), "
+        "hashlib.sha256(out.tobytes()).hexdigest())\n")
+    words, answers = _run_with_env(script, **env).split()
+    assert words == case["words_sha256"]
+    assert answers == case["out_sha256"]
