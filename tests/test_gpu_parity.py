@@ -104,6 +104,13 @@ def test_relaxed_build_tolerance(golden, name):
     hist = bb.block_load_histogram(f)
     assert abs(hist.mean_load - case["mean_load"]) <= max(1.0, 0.01 * case["mean_load"])
     assert abs(hist.variance / case["variance"] - 1) <= 0.15 + 0.3 * (f.num_blocks < 1000)
+    if f.num_blocks >= 4096:
+        # load-histogram total variation vs the exact build (<= 0.05)
+        exact = bb.Filter.from_config(config_of(case))
+        exact.insert_many(keys)
+        assert sha(exact.storage.words) == case["words_sha256"]
+        tv = bb.histogram_distance(hist.counts, bb.block_load_histogram(exact).counts)
+        assert tv <= 0.05, tv
 
 
 def test_relaxed_equals_ordered_for_single_choice(golden):
