@@ -225,6 +225,69 @@ __global__ void __launch_bounds__(kTPB) lookup512_pipe_kernel(const __grid_const
     }
 }
 
+// Multi-choice lookups with the next tile's first choice in flight: the
+// choice-0 blocks of tile t+1 are staged (one cp.async group) before tile t is
+// tested; tile t's later choices -- only for its still-pending keys, the
+// reference's early exit -- are staged into tile t's own buffer once its
+// choice-0 test is done.
+template <int C, int K>
+__global__ void __launch_bounds__(kTPB) lookup512_pipe_multi_kernel(
+    const __grid_constant__ KParams p, const u64 *__restrict__ words,
+    const u64 *__restrict__ keys, u64 n, u8 *__restrict__ out,
+    unsigned long long *__restrict__ hits) {
+    __shared__ PipeStage stages[kWarps][2];
+    PipeStage *st = stages[threadIdx.x >> 5];
+    const int lane = threadIdx.x & 31;
+    const u64 ntiles = (n + 31) / 32;
+    const u64 nwarps = (u64)gridDim.x * kWarps;
+    u32 my_hits = 0;
+    u64 tile = blockIdx.x * (u64)kWarps + (threadIdx.x >> 5);
+    u64 i = tile * 32 + lane;
+    bool valid = i < n;
+    u64 x = valid ? ld_stream(keys + i) : 0ull;
+    stage_blocks(words, st[0], valid ? (u32)block_index(p, x, 0) : 0u,
+                 __ballot_sync(kFull, valid), lane);
+    u64 tile_n = tile + nwarps;
+    i = tile_n * 32 + lane;
+    u64 x_n = i < n ? ld_stream(keys + i) : 0ull;
+    int b = 0;
+    for (; tile < ntiles; tile = tile_n, tile_n += nwarps) {
+        const u64 base = tile * 32;
+        const bool valid_n = tile_n * 32 + lane < n;
+        stage_blocks(words, st[b ^ 1], valid_n ? (u32)block_index(p, x_n, 0) : 0u,
+                     __ballot_sync(kFull, valid_n), lane);
+        i = (tile_n + nwarps) * 32 + lane;
+        const u64 x_nn = i < n ? ld_stream(keys + i) : 0ull;
+        asm volatile("cp.async.wait_group 1;" ::: "memory");
+        __syncwarp();
+        bool f = valid && test_staged<K>(p, st[b], x, lane);
+        u32 done = __ballot_sync(kFull, !valid || f);
+#pragma unroll
+        for (int ci = 1; ci < C; ++ci) {
+            if (done == kFull) break;
+            __syncwarp();  // every lane is done reading st[b]
+            const bool pend = !((done >> lane) & 1u);
+            stage_blocks(words, st[b], pend ? (u32)block_index(p, x, ci) : 0u, ~done, lane);
+            asm volatile("cp.async.wait_group 0;" ::: "memory");
+            __syncwarp();
+            if (pend) f = test_staged<K>(p, st[b], x, lane);
+            done |= __ballot_sync(kFull, f);
+        }
+        if (out != nullptr && valid) out[base + lane] = (u8)f;
+        my_hits += f ? 1u : 0u;
+        __syncwarp();
+        x = x_n;
+        x_n = x_nn;
+        valid = valid_n;
+        b ^= 1;
+    }
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    if (hits != nullptr) {
+        for (int o = 16; o > 0; o >>= 1) my_hits += __shfl_xor_sync(kFull, my_hits, o);
+        if (lane == 0 && my_hits) atomicAdd(hits, (unsigned long long)my_hits);
+    }
+}
+
 template <int OP>
 __global__ void __launch_bounds__(256) generic_kernel(const __grid_constant__ KParams p,
                                                       u64 *__restrict__ words,
@@ -665,6 +728,12 @@ static cudaError_t launch_pipe(const KParams &p, const u64 *words, const u64 *ke
 template <int C, int K>
 static cudaError_t launch_lookup_k(const KParams &p, const u64 *words, const u64 *keys, u64 n,
                                    u8 *out, unsigned long long *hits, cudaStream_t s) {
+    if (C <= 3 && lookup_pipe_enabled()) {
+        const void *fp = (const void *)lookup512_pipe_multi_kernel<C, K>;
+        const unsigned g = grid_for(fp, kTPB, 0, (n + kTPB - 1) / kTPB);
+        return launch_words(lookup512_pipe_multi_kernel<C, K>, g, p, words, s, p, words, keys, n,
+                            out, hits);
+    }
     const void *fl = (const void *)lookup512_kernel<C, K>;
     const unsigned g = grid_for(fl, kTPB, 0, (n + kTPB - 1) / kTPB);
     return launch_words(lookup512_kernel<C, K>, g, p, words, s, p, words, keys, n, out, hits);
