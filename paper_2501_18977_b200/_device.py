@@ -27,12 +27,32 @@ def stream_ptr(device: torch.device | None = None) -> int:
     return torch.cuda.current_stream(device).cuda_stream
 
 
+def _foreign_cuda(x):
+    """Zero-copy torch view of a non-torch CUDA array (__cuda_array_interface__
+    or DLPack on a CUDA device, e.g. CuPy / Numba / JAX arrays), else None."""
+    if isinstance(x, (torch.Tensor, np.ndarray)):
+        return None
+    if hasattr(x, "__cuda_array_interface__"):
+        return torch.as_tensor(x, device="cuda")
+    if hasattr(x, "__dlpack__") and hasattr(x, "__dlpack_device__"):
+        dev_type, _ = x.__dlpack_device__()
+        if int(dev_type) in (2, 13):  # kDLCUDA, kDLCUDAManaged
+            return torch.from_dlpack(x)
+    return None
+
+
 def is_device_tensor(x) -> bool:
-    return isinstance(x, torch.Tensor) and x.is_cuda
+    """CUDA input: a CUDA torch tensor or any array exposing CUDA memory."""
+    if isinstance(x, torch.Tensor):
+        return x.is_cuda
+    return _foreign_cuda(x) is not None
 
 
 def as_device_u64(x, device: torch.device) -> torch.Tensor:
     """A contiguous uint64 CUDA tensor holding the keys of ``x``."""
+    foreign = _foreign_cuda(x)
+    if foreign is not None:
+        x = foreign
     if isinstance(x, torch.Tensor):
         if x.dtype == torch.int64:
             x = x.view(torch.uint64)

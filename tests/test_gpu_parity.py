@@ -553,3 +553,38 @@ def test_fallback_kernels_match_reference(golden, name, env):
     words, answers = _run_with_env(script, **env).split()
     assert words == case["words_sha256"]
     assert answers == case["out_sha256"]
+
+
+def test_foreign_cuda_arrays_stay_on_device(golden):
+    """Keys given as non-torch CUDA arrays (__cuda_array_interface__ or
+    DLPack, as CuPy / Numba provide) are used in place and answered on the
+    device, like CUDA tensors."""
+    meta, _ = golden
+    case = meta["cfg1"]
+    keys, probes = probes_of(case)
+    t_keys = torch.from_numpy(keys).cuda()
+    t_probes = torch.from_numpy(probes).cuda()
+
+    class CAI:
+        def __init__(self, t):
+            self.t = t
+            self.__cuda_array_interface__ = t.__cuda_array_interface__
+
+    class DL:
+        def __init__(self, t):
+            self.t = t
+
+        def __dlpack__(self, stream=None):
+            return self.t.__dlpack__()
+
+        def __dlpack_device__(self):
+            return self.t.__dlpack_device__()
+
+    for wrap in (CAI, DL):
+        f = bb.Filter.from_config(config_of(case))
+        f.insert_many(wrap(t_keys))
+        assert sha(f.storage.words) == case["words_sha256"]
+        out = f.contains_many(wrap(t_probes))
+        assert isinstance(out, torch.Tensor) and out.is_cuda
+        assert sha(out.cpu().numpy().astype(np.uint8)) == case["out_sha256"]
+        assert f.count_hits(wrap(t_probes)) == case["hits_pos"] + case["hits_neg"]
