@@ -170,6 +170,19 @@ BC_API int bc_pcg64_fill(uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi, 
 BC_API int bc_format_answers(const uint64_t *h_keys, const uint8_t *h_answers, uint64_t n,
                              char *h_out, uint64_t out_cap, uint64_t *written);
 
+/* Host-side text key ingestion (read_keys(..., "text"), io.py:206-223): parses
+ * the complete lines of h_text[0, len) -- one decimal key per line, surrounding
+ * ASCII whitespace and blank lines ignored, an optional sign and single
+ * underscores between digits accepted, as Python's int() does -- into h_keys
+ * (capacity cap).  Parsing stops after the last '\n' (the caller carries the
+ * partial tail) or when cap keys are stored.  *consumed = bytes of h_text
+ * used, *lines = lines used, *n_keys = keys stored.  A line that is not an
+ * integer, or whose value is outside [0, 2^64), stops the parse with
+ * BC_EINVAL; *lines is then the 0-based index of that line among the ones
+ * given (the caller re-reads it to word the error). */
+BC_API int bc_parse_keys_text(const char *h_text, uint64_t len, uint64_t *h_keys, uint64_t cap,
+                              uint64_t *consumed, uint64_t *lines, uint64_t *n_keys);
+
 /* Thread-local description of the last error on this thread. */
 BC_API const char *bc_last_error(void);
 

@@ -26,7 +26,7 @@ EXPORTS = (
     "bc_insert_host", "bc_contains_host", "bc_encode_qgrams", "bc_insert_qgrams",
     "bc_contains_qgrams", "bc_block_histogram", "bc_route", "bc_eval_hash",
     "bc_last_error", "bc_launch_count", "bc_version", "bc_pcg64_fill", "bc_l2_release",
-    "bc_format_answers",
+    "bc_format_answers", "bc_parse_keys_text",
 )
 
 
@@ -93,13 +93,14 @@ def lib() -> ctypes.CDLL:
         L.bc_version.restype = ctypes.c_char_p
         L.bc_l2_release.restype = None
         L.bc_format_answers.argtypes = [P, P, u64, P, u64, P]
+        L.bc_parse_keys_text.argtypes = [P, u64, P, u64, P, P, P]
         for name in EXPORTS:
             fn = getattr(L, name)
             if fn.restype is ctypes.c_int or name in (
                     "bc_filter_create", "bc_insert", "bc_contains", "bc_insert_host",
                     "bc_contains_host", "bc_encode_qgrams", "bc_insert_qgrams",
                     "bc_contains_qgrams", "bc_block_histogram", "bc_route", "bc_eval_hash",
-                    "bc_pcg64_fill", "bc_format_answers"):
+                    "bc_pcg64_fill", "bc_format_answers", "bc_parse_keys_text"):
                 fn.restype = ctypes.c_int
         _lib = L
         atexit.register(L.bc_l2_release)

@@ -605,6 +605,76 @@ extern "C" int bc_format_answers(const uint64_t *h_keys, const uint8_t *h_answer
     return BC_OK;
 }
 
+// ---- text key ingestion ---------------------------------------------------------------
+namespace {
+inline bool is_space(char c) {
+    return c == ' ' || c == '\t' || c == '\r' || c == '\v' || c == '\f' || c == '\n';
+}
+
+// One stripped, non-empty line -> value; false if int() would reject it or the
+// value is outside [0, 2^64).
+bool parse_line(const char *b, const char *e, u64 *v) {
+    bool neg = false;
+    if (*b == '+' || *b == '-') {
+        neg = *b == '-';
+        ++b;
+    }
+    if (b == e) return false;
+    u64 acc = 0;
+    bool prev_digit = false;
+    for (const char *c = b; c < e; ++c) {
+        if (*c == '_') {  // only between two digits
+            if (!prev_digit || c + 1 == e || c[1] < '0' || c[1] > '9') return false;
+            prev_digit = false;
+            continue;
+        }
+        if (*c < '0' || *c > '9') return false;
+        const u64 d = (u64)(*c - '0');
+        if (acc > (~0ull - d) / 10) return false;  // >= 2^64
+        acc = acc * 10 + d;
+        prev_digit = true;
+    }
+    if (neg && acc != 0) return false;  // negative
+    *v = acc;
+    return true;
+}
+}  // namespace
+
+extern "C" int bc_parse_keys_text(const char *h_text, uint64_t len, uint64_t *h_keys,
+                                  uint64_t cap, uint64_t *consumed, uint64_t *lines,
+                                  uint64_t *n_keys) {
+    if (!consumed || !lines || !n_keys) return fail(BC_EINVAL, "null output counters");
+    *consumed = *lines = *n_keys = 0;
+    if (len && !h_text) return fail(BC_EINVAL, "null text");
+    if (cap && !h_keys) return fail(BC_EINVAL, "null key buffer");
+    const char *p = h_text, *end = h_text + len;
+    u64 n = 0, line = 0;
+    while (p < end && n < cap) {
+        const char *nl = static_cast<const char *>(std::memchr(p, '\n', (size_t)(end - p)));
+        if (!nl) break;  // partial line: the caller carries it
+        const char *b = p, *e = nl;
+        while (b < e && is_space(*b)) ++b;
+        while (e > b && is_space(e[-1])) --e;
+        if (b < e) {
+            u64 v;
+            if (!parse_line(b, e, &v)) {
+                *consumed = (u64)(p - h_text);
+                *lines = line;
+                *n_keys = n;
+                return fail(BC_EINVAL, "line %llu of the chunk is not a 64-bit key",
+                            (unsigned long long)line);
+            }
+            h_keys[n++] = v;
+        }
+        ++line;
+        p = nl + 1;
+    }
+    *consumed = (u64)(p - h_text);
+    *lines = line;
+    *n_keys = n;
+    return BC_OK;
+}
+
 // ---- host-buffer entry points ---------------------------------------------------------
 // Per-device staging: two pinned key buffers, two pinned answer buffers, two
 // device key/answer buffers and two copy streams, so the copy of chunk i+1

@@ -20,12 +20,14 @@ a second full host copy.  Hash functions are re-derived from the stored seed.
 
 from __future__ import annotations
 
+import ctypes
 import struct
 import sys
 from typing import BinaryIO, Iterator
 
 import numpy as np
 
+from . import _native
 from .filters import CostModel, Filter
 from .qgrams import QGramEncoder, encode_qgrams, join_records
 
@@ -145,38 +147,78 @@ def _open_binary(path) -> BinaryIO:
 
 
 def _read_u64le(fh: BinaryIO, chunk: int) -> Iterator[np.ndarray]:
-    tail = b""
+    """Raw little-endian records; short reads (pipes) are topped up, and a
+    stream whose length is not a multiple of 8 is an error (io.py:191-203)."""
+    buf = bytearray()
+    want = chunk * 8
     while True:
-        data = fh.read(chunk * 8)
-        if not data:
+        got = fh.read(want - len(buf))
+        if got:
+            buf += got
+        if len(buf) >= want or (not got and len(buf) >= 8):
+            whole = len(buf) - len(buf) % 8
+            yield np.frombuffer(bytes(buf[:whole]), dtype="<u8").astype(np.uint64)
+            del buf[:whole]
+        if not got:
             break
-        data = tail + data
-        cut = len(data) - len(data) % 8
-        if cut:
-            yield np.frombuffer(data[:cut], dtype="<u8").astype(np.uint64)
-        tail = data[cut:]
-    if tail:
-        raise KeyFormatError(f"u64le stream truncated ({len(tail)} stray bytes)")
+    if buf:
+        raise KeyFormatError(f"u64le stream truncated ({len(buf)} stray bytes)")
+
+
+_TEXT_BLOCK = 1 << 24  # bytes per native parse call
+
+
+def _text_error(line: bytes, lineno: int) -> KeyFormatError:
+    """The reference's wording for a rejected line (io.py:206-223)."""
+    line = line.strip()
+    try:
+        value = int(line)
+    except ValueError:
+        return KeyFormatError(f"line {lineno}: not an integer: {line!r}")
+    return KeyFormatError(f"line {lineno}: key out of 64-bit range: {value}")
 
 
 def _read_text(fh: BinaryIO, chunk: int) -> Iterator[np.ndarray]:
-    batch: list = []
-    for lineno, line in enumerate(fh, start=1):
-        line = line.strip()
-        if not line:
-            continue
-        try:
-            v = int(line)
-        except ValueError as exc:
-            raise KeyFormatError(f"line {lineno}: not an integer: {line!r}") from exc
-        if not 0 <= v < 2**64:
-            raise KeyFormatError(f"line {lineno}: key out of 64-bit range: {v}")
-        batch.append(v)
-        if len(batch) >= chunk:
-            yield np.array(batch, dtype=np.uint64)
-            batch = []
-    if batch:
-        yield np.array(batch, dtype=np.uint64)
+    """One decimal key per line, parsed natively (bc_parse_keys_text) in
+    blocks of whole lines; keys are yielded in batches of up to ``chunk``."""
+    lib = _native.lib()
+    out = np.empty(chunk, dtype=np.uint64)
+    used = ctypes.c_uint64()
+    nlines = ctypes.c_uint64()
+    nkeys = ctypes.c_uint64()
+    fill = 0
+    lineno = 1  # number of the first line still to parse
+    tail = b""
+    eof = False
+    while not eof:
+        data = fh.read(_TEXT_BLOCK)
+        eof = not data
+        text = tail + data
+        if eof:
+            if not text:
+                break
+            text += b"\n"  # the last line needs no newline
+        view = np.frombuffer(text, dtype=np.uint8)
+        off = 0
+        while off < len(text):
+            rc = lib.bc_parse_keys_text(view.ctypes.data + off, len(text) - off,
+                                        out.ctypes.data + 8 * fill, chunk - fill,
+                                        ctypes.byref(used), ctypes.byref(nlines),
+                                        ctypes.byref(nkeys))
+            fill += nkeys.value
+            if rc != _native.BC_OK:
+                start = off + used.value
+                stop = text.find(b"\n", start)
+                raise _text_error(text[start:stop], lineno + nlines.value)
+            off += used.value
+            lineno += nlines.value
+            if fill < chunk:
+                break  # every whole line is parsed; a partial one may remain
+            yield out.copy()
+            fill = 0
+        tail = text[off:]
+    if fill:
+        yield out[:fill].copy()
 
 
 def fasta_records(fh: BinaryIO) -> Iterator[bytes]:

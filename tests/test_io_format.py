@@ -181,3 +181,59 @@ def test_gpu_filter_roundtrip_and_fasta(tmp_path):
     assert len(chunks) == 2
     np.testing.assert_array_equal(chunks[0], orc.encode_qgrams(b"ACGTACGTACGTTTACG", 5))
     np.testing.assert_array_equal(chunks[1], orc.encode_qgrams(b"NNACGTAAAC", 5))
+
+
+def _python_keys(text: bytes):
+    """The reference's text rule (io.py:206-223) restated in Python."""
+    keys = []
+    for line in text.split(b"\n"):
+        line = line.strip()
+        if line:
+            keys.append(int(line))
+    return keys
+
+
+@pytest.mark.parametrize("block", [7, 64, 1 << 24])
+def test_native_text_parser_matches_python_int(tmp_path, monkeypatch, block):
+    """bc_parse_keys_text accepts exactly what int() accepts (sign, leading
+    zeros, single underscores, surrounding whitespace, CRLF, blank lines),
+    across read-block boundaries and output chunks."""
+    import paper_2501_18977_b200.io as bio
+
+    monkeypatch.setattr(bio, "_TEXT_BLOCK", block)
+    rng = np.random.default_rng(9)
+    vals = rng.integers(0, 2**64, size=500, dtype=np.uint64).tolist()
+    forms = []
+    for i, v in enumerate(vals):
+        s = str(v)
+        kind = i % 7
+        if kind == 1:
+            s = "+" + s
+        elif kind == 2:
+            s = "000" + s
+        elif kind == 3 and len(s) > 3:
+            s = s[:2] + "_" + s[2:]
+        elif kind == 4:
+            s = " \t" + s + " \r"
+        elif kind == 5:
+            s = s + "\n"  # a blank line follows
+        forms.append(s)
+    forms += ["-0", "0", str(2**64 - 1), "1_0_0"]
+    text = ("\n".join(forms)).encode()  # no trailing newline
+    p = tmp_path / "k.txt"
+    p.write_bytes(text)
+    got = np.concatenate(list(read_keys(str(p), "text", chunk_size=37)))
+    assert got.tolist() == _python_keys(text)
+
+
+@pytest.mark.parametrize("bad,msg", [
+    (b"1__0", "line 3: not an integer"), (b"_1", "line 3: not an integer"),
+    (b"1_", "line 3: not an integer"), (b"0x10", "line 3: not an integer"),
+    (b"1 2", "line 3: not an integer"), (b"-1", "line 3: key out of 64-bit range: -1"),
+    (str(2**64).encode(), f"line 3: key out of 64-bit range: {2**64}"),
+])
+def test_native_text_parser_errors(tmp_path, bad, msg):
+    p = tmp_path / "k.txt"
+    p.write_bytes(b"5\n\n" + bad + b"\n7\n")
+    with pytest.raises(KeyFormatError, match=msg.replace("+", r"\+")):
+        list(read_keys(str(p), "text"))
