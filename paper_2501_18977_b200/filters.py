@@ -149,59 +149,71 @@ class FilterConfig:
     seed: int = 0
     block_bits: int = 512
 
-    def validated(self) -> "FilterConfig":
-        if self.kind not in KINDS:
-            raise ConfigError(f"unknown filter kind {self.kind!r}")
-        if not valid_block_bits(self.block_bits):
-            raise ConfigError(f"invalid block_bits {self.block_bits}")
-        if not 1 <= self.k <= self.block_bits:
-            raise ConfigError(f"k must be in [1, {self.block_bits}] for {self.block_bits}-bit "
-                              f"blocks, got {self.k}")
-        if self.strategy not in ("random", "distinct"):
-            raise ConfigError(f"unknown bit strategy {self.strategy!r}")
-        if (self.n_capacity is None) == (self.size_bits is None):
-            raise ConfigError("give exactly one of n_capacity and size_bits")
-        if self.n_capacity is not None and self.n_capacity < 1:
-            raise ConfigError(f"capacity must be >= 1, got {self.n_capacity}")
-        if self.size_bits is not None:
-            if self.size_bits < 1:
-                raise ConfigError(f"size_bits must be >= 1, got {self.size_bits}")
-            if self.relative_size != 1.0:
-                raise ConfigError("relative_size only applies to capacity-based sizing")
-        if not self.relative_size > 0:
-            raise ConfigError(f"relative_size must be > 0, got {self.relative_size}")
-        if self.shards < 1:
-            raise ConfigError(f"shard count must be >= 1, got {self.shards}")
-        choices, cost = self.choices, self.cost
+    def _problems(self):
+        """The configuration errors, in the order the reference checks them
+        (filters.py:147-194): (condition, message) pairs, lazily."""
+        bb = self.block_bits
+        yield self.kind not in KINDS, lambda: f"unknown filter kind {self.kind!r}"
+        yield not valid_block_bits(bb), lambda: f"invalid block_bits {bb}"
+        yield not 1 <= self.k <= bb, \
+            lambda: f"k must be in [1, {bb}] for {bb}-bit blocks, got {self.k}"
+        yield self.strategy not in ("random", "distinct"), \
+            lambda: f"unknown bit strategy {self.strategy!r}"
+        yield (self.n_capacity is None) == (self.size_bits is None), \
+            lambda: "give exactly one of n_capacity and size_bits"
+        yield self.n_capacity is not None and self.n_capacity < 1, \
+            lambda: f"capacity must be >= 1, got {self.n_capacity}"
+        sized = self.size_bits is not None
+        yield sized and self.size_bits < 1, lambda: f"size_bits must be >= 1, got {self.size_bits}"
+        yield sized and self.relative_size != 1.0, \
+            lambda: "relative_size only applies to capacity-based sizing"
+        yield not self.relative_size > 0, \
+            lambda: f"relative_size must be > 0, got {self.relative_size}"
+        yield self.shards < 1, lambda: f"shard count must be >= 1, got {self.shards}"
+
+    def _per_kind(self) -> tuple:
+        """(choices, cost) normalised for the kind, or ConfigError."""
+        c, cost = self.choices, self.cost
         if self.kind == "standard":
-            if self.strategy != "random":
-                raise ConfigError("the distinct strategy applies only to blocked filters")
-            if self.shards != 1:
-                raise ConfigError("standard filters do not shard (bits span the whole array)")
-            if self.block_bits % 64 != 0:
-                raise ConfigError("standard filters need word-multiple block_bits")
-            choices, cost = 0, None
-        elif self.kind == "blocked":
-            if choices not in (None, 1):
-                raise ConfigError(f"blocked filters have exactly one choice, got {choices}")
-            choices, cost = 1, None
-        else:
-            choices = 2 if choices is None else choices
-            if not 2 <= choices <= MAX_CHOICES:
-                raise ConfigError(
-                    f"blowchoc needs between 2 and {MAX_CHOICES} choices, got {choices}")
-            cost = default_cost(self.k) if cost is None else cost
-            if cost.k != self.k:
-                raise ConfigError(f"cost model k={cost.k} does not match filter k={self.k}")
-        return replace(self, choices=choices, cost=cost, seed=self.seed & ((1 << 64) - 1))
+            checks = ((self.strategy != "random",
+                       "the distinct strategy applies only to blocked filters"),
+                      (self.shards != 1,
+                       "standard filters do not shard (bits span the whole array)"),
+                      (self.block_bits % 64 != 0,
+                       "standard filters need word-multiple block_bits"))
+            for bad, msg in checks:
+                if bad:
+                    raise ConfigError(msg)
+            return 0, None
+        if self.kind == "blocked":
+            if c not in (None, 1):
+                raise ConfigError(f"blocked filters have exactly one choice, got {c}")
+            return 1, None
+        c = 2 if c is None else c
+        if not 2 <= c <= MAX_CHOICES:
+            raise ConfigError(f"blowchoc needs between 2 and {MAX_CHOICES} choices, got {c}")
+        cost = cost if cost is not None else default_cost(self.k)
+        if cost.k != self.k:
+            raise ConfigError(f"cost model k={cost.k} does not match filter k={self.k}")
+        return c, cost
+
+    def validated(self) -> "FilterConfig":
+        """A normalised copy (choices and cost filled in per kind, 64-bit seed),
+        or ConfigError with the reference's message."""
+        for bad, message in self._problems():
+            if bad:
+                raise ConfigError(message())
+        choices, cost = self._per_kind()
+        return replace(self, choices=choices, cost=cost, seed=self.seed % (1 << 64))
 
     def sizing(self) -> tuple:
-        if self.size_bits is not None:
-            blocks = -(-self.size_bits // self.block_bits)
-            blocks = -(-blocks // self.shards) * self.shards
-            return blocks * self.block_bits, blocks
-        return size_for(self.n_capacity, self.k, self.relative_size, self.block_bits,
-                        self.shards)
+        """(m bits, M blocks): ``size_bits`` rounded up to whole blocks and a
+        shard multiple, else ``size_for`` of the capacity."""
+        if self.size_bits is None:
+            return size_for(self.n_capacity, self.k, self.relative_size, self.block_bits,
+                            self.shards)
+        blocks = -(-self.size_bits // (self.block_bits * self.shards)) * self.shards
+        return blocks * self.block_bits, blocks
 
 
 _KIND_CODE = {"standard": 0, "blocked": 1, "blowchoc": 2}

@@ -287,7 +287,44 @@ def bwch_files() -> None:
         json.dump(meta, fh, indent=1)
 
 
+def config_cases() -> None:
+    """FilterConfig.validated / sizing outcomes of the reference on seeded
+    random (mostly invalid) parameter sets: error class and message, or the
+    normalised choices / seed and the sizing (config_cases.json)."""
+    import random
+
+    rng = random.Random(5)
+    grid = dict(kind=["standard", "blocked", "blowchoc", "bogus"], k=[0, 1, 7, 600],
+                n_capacity=[None, 0, 1000, 123457], size_bits=[None, 0, 5000, 99991],
+                choices=[None, 0, 1, 2, 3, 9], strategy=["random", "distinct", "x"],
+                relative_size=[1.0, 0.0, 1.3], shards=[0, 1, 4, 7],
+                seed=[0, 2**70 + 3, -5], block_bits=[512, 64, 100, 16, 1024])
+    tame = dict(kind=["standard", "blocked", "blowchoc", "blowchoc"], k=[1, 7, 12, 16],
+                choices=[None, 2, 3, 8], strategy=["random", "random", "distinct"],
+                shards=[1, 1, 4, 7], seed=[0, 1, 2**70 + 3], block_bits=[512, 512, 64, 1024])
+    cases = []
+    for i in range(1500):
+        if i % 3:  # mostly plausible configurations, sized one way or the other
+            kw = {name: rng.choice(v) for name, v in tame.items()}
+            if rng.random() < 0.5:
+                kw["n_capacity"] = rng.randrange(1, 10**7)
+                kw["relative_size"] = rng.choice([1.0, 0.8, 1.25])
+            else:
+                kw["size_bits"] = rng.randrange(1, 10**9)
+        else:
+            kw = {name: rng.choice(v) for name, v in grid.items()}
+        try:
+            c = FilterConfig(**kw).validated()
+            res = {"ok": True, "choices": c.choices, "seed": c.seed, "sizing": list(c.sizing())}
+        except Exception as exc:  # noqa: BLE001 -- the class and message are the fixture
+            res = {"ok": False, "error": type(exc).__name__, "message": str(exc)}
+        cases.append({"config": kw, "result": res})
+    with open(os.path.join(OUT, "config_cases.json"), "w") as fh:
+        json.dump(cases, fh, separators=(",", ":"))
+
+
 def main() -> None:
+    config_cases()
     bwch_files()
     store: dict = {}
     meta: dict = {}

@@ -208,3 +208,26 @@ def test_partition_by_shard_is_stable():
     shard = np.array([i % 3 for i in range(20)], dtype=np.uint64)
     parts = partition_by_shard(keys, shard, 3)
     assert [p.tolist() for p in parts] == [list(range(s, 20, 3)) for s in range(3)]
+
+
+def test_config_validation_matches_reference_fixture():
+    """FilterConfig.validated / sizing against the reference's own outcomes on
+    1500 seeded parameter sets (tests/golden/config_cases.json, written by
+    make_golden.py): the same error class and message, or the same
+    normalised choices, seed and sizing."""
+    import json
+    import os
+
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden",
+                        "config_cases.json")
+    with open(path) as fh:
+        cases = json.load(fh)
+    assert len(cases) == 1500
+    for case in cases:
+        want = case["result"]
+        try:
+            c = bb.FilterConfig(**case["config"]).validated()
+            got = {"ok": True, "choices": c.choices, "seed": c.seed, "sizing": list(c.sizing())}
+        except Exception as exc:  # noqa: BLE001
+            got = {"ok": False, "error": type(exc).__name__, "message": str(exc)}
+        assert got == want, case["config"]
