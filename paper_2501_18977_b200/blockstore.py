@@ -96,43 +96,47 @@ class BlockArray:
     def total_bits(self) -> int:
         return self.num_blocks * self.block_bits
 
-    # -- scalar primitives (host mirror; the reference's scalar API) ----------------
-    def _check(self, block: int, addrs=()) -> None:
+    # -- scalar primitives on the host mirror (the reference's per-key API) ---------
+    def _addresses(self, block: int, addrs) -> np.ndarray:
+        """Validated bit addresses as an int64 array (IndexError like the
+        reference for a bad block or address)."""
         if not 0 <= block < self.num_blocks:
             raise IndexError(f"block {block} out of range [0, {self.num_blocks})")
-        for a in addrs:
-            if not 0 <= a < self.block_bits:
-                raise IndexError(f"bit address {a} out of range [0, {self.block_bits})")
+        vals = [int(v) for v in addrs]
+        first_bad = next((v for v in vals if not 0 <= v < self.block_bits), None)
+        if first_bad is not None:
+            raise IndexError(f"bit address {first_bad} out of range [0, {self.block_bits})")
+        return np.array(vals, dtype=np.int64)
 
-    def _mask(self, addrs) -> np.ndarray:
+    def _mask_of(self, a: np.ndarray) -> np.ndarray:
         m = np.zeros(self.words_per_block, dtype=np.uint64)
-        for a in addrs:
-            m[a >> 6] |= np.uint64(1) << np.uint64(a & 63)
+        np.bitwise_or.at(m, a >> 6, np.left_shift(np.uint64(1), (a & 63).astype(np.uint64)))
         return m
 
     def block_words(self, block: int) -> np.ndarray:
-        w = self.words_per_block
-        return self.words[block * w:(block + 1) * w]
+        """Writable view of one block's words on the host mirror."""
+        lo = block * self.words_per_block
+        return self.words[lo:lo + self.words_per_block]
 
     def set_bits(self, block: int, addrs) -> None:
-        self._check(block, addrs)
-        self.block_words(block)[:] |= self._mask(addrs)
+        m = self._mask_of(self._addresses(block, addrs))
+        np.bitwise_or(self.block_words(block), m, out=self.block_words(block))
 
     def test_all(self, block: int, addrs) -> bool:
-        self._check(block, addrs)
-        m = self._mask(addrs)
-        return bool(np.all((self.block_words(block) & m) == m))
+        m = self._mask_of(self._addresses(block, addrs))
+        return not np.any(m & ~self.block_words(block))
 
     def popcount_block(self, block: int) -> int:
-        self._check(block)
-        return int(popcount_words(self.block_words(block)).sum())
+        self._addresses(block, ())
+        return int(np.bitwise_count(self.block_words(block)).sum())
 
     def simulate_insertion(self, block: int, addrs) -> tuple:
-        self._check(block, addrs)
+        """(j, a): set bits after inserting ``addrs`` and how many of them are
+        new; the block is left untouched (a == 0: all already set)."""
+        m = self._mask_of(self._addresses(block, addrs))
         view = self.block_words(block)
-        m = self._mask(addrs)
-        j = int(popcount_words(view | m).sum())
-        return j, j - int(popcount_words(view).sum())
+        new = int(np.bitwise_count(m & ~view).sum())
+        return int(np.bitwise_count(view).sum()) + new, new
 
     def histogram(self) -> np.ndarray:
         """counts[j] = blocks with j set bits, on the GPU."""

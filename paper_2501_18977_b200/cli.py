@@ -165,55 +165,63 @@ def cmd_hist(args) -> int:
     return EXIT_OK
 
 
-def _add_key_input(p, required=True):
-    p.add_argument("--keys", required=required, help="key file, '-' for stdin")
-    p.add_argument("--format", default="u64le", choices=["u64le", "text", "fasta"])
-    p.add_argument("--q", type=int, default=None, help="q-gram length for fasta")
-    p.add_argument("--no-canonical", action="store_true",
-                   help="keep q-grams strand-specific")
+# Command table: the reference's flags (cli.py:253-330) for the filter
+# commands, as (flags, argparse keywords).  "@keys" / "@keys?" expand to the
+# key-stream options (required / optional).
+_KEY_INPUT = [
+    ("--keys", dict(help="key file, '-' for stdin")),
+    ("--format", dict(default="u64le", choices=["u64le", "text", "fasta"])),
+    ("--q", dict(type=int, default=None, help="q-gram length for fasta")),
+    ("--no-canonical", dict(action="store_true", help="keep q-grams strand-specific")),
+]
+_GPU_THREADS = ("--threads", dict(type=int, default=1, help="accepted; lookups run on the GPU"))
+_COMMANDS = {
+    "build": ("build a filter from a key stream", [
+        ("--kind", dict(required=True, choices=["standard", "blocked", "blowchoc"])),
+        ("--k", dict(type=int, required=True, help="bit address functions per key")),
+        ("--choices", dict(type=int, default=None)),
+        ("--n", dict(type=int, default=None, help="planned key count")),
+        ("--size-bits", dict(type=int, default=None, help="filter size in bits instead of --n")),
+        ("--relative-size", dict(type=float, default=1.0)),
+        ("--cost", dict(choices=["exp", "mix", "la"], default=None)),
+        ("--cost-param", dict(type=float, default=None)),
+        ("--strategy", dict(choices=["random", "distinct"], default="random")),
+        ("--threads", dict(type=int, default=0,
+                           help="shards (the reference's worker threads); 0 = unsharded")),
+        ("--seed", dict(type=int, default=0)),
+        "@keys",
+        ("--out", dict(required=True)),
+    ], {}),
+    "query": ("query keys against a stored filter",
+              [("--filter", dict(required=True)), "@keys", _GPU_THREADS], {}),
+    "fpr": ("estimate the empirical FPR of a filter", [
+        ("--filter", dict(required=True)),
+        ("--negatives", dict(type=int, default=10**6,
+                             help="generated negative queries (odd keys)")),
+        ("--neg-seed", dict(type=int, default=0xFEEDBEEF)),
+        _GPU_THREADS,
+        "@keys?",
+    ], {"keys": None}),
+    "hist": ("per-block load histogram of a filter", [("--filter", dict(required=True))], {}),
+}
+_HANDLERS = {"build": lambda a: cmd_build(a), "query": lambda a: cmd_query(a),
+             "fpr": lambda a: cmd_fpr(a), "hist": lambda a: cmd_hist(a)}
 
 
 def build_parser() -> argparse.ArgumentParser:
     parser = _Parser(prog="paper_2501_18977_b200", description=__doc__,
                      formatter_class=argparse.RawDescriptionHelpFormatter)
     sub = parser.add_subparsers(dest="command", required=True)
-
-    p = sub.add_parser("build", help="build a filter from a key stream")
-    p.add_argument("--kind", required=True, choices=["standard", "blocked", "blowchoc"])
-    p.add_argument("--k", type=int, required=True, help="bit address functions per key")
-    p.add_argument("--choices", type=int, default=None)
-    p.add_argument("--n", type=int, default=None, help="planned key count")
-    p.add_argument("--size-bits", type=int, default=None,
-                   help="filter size in bits instead of --n")
-    p.add_argument("--relative-size", type=float, default=1.0)
-    p.add_argument("--cost", choices=["exp", "mix", "la"], default=None)
-    p.add_argument("--cost-param", type=float, default=None)
-    p.add_argument("--strategy", choices=["random", "distinct"], default="random")
-    p.add_argument("--threads", type=int, default=0,
-                   help="shards (the reference's worker threads); 0 = unsharded")
-    p.add_argument("--seed", type=int, default=0)
-    _add_key_input(p)
-    p.add_argument("--out", required=True)
-    p.set_defaults(func=cmd_build)
-
-    p = sub.add_parser("query", help="query keys against a stored filter")
-    p.add_argument("--filter", required=True)
-    _add_key_input(p)
-    p.add_argument("--threads", type=int, default=1, help="accepted; lookups run on the GPU")
-    p.set_defaults(func=cmd_query)
-
-    p = sub.add_parser("fpr", help="estimate the empirical FPR of a filter")
-    p.add_argument("--filter", required=True)
-    p.add_argument("--negatives", type=int, default=10**6,
-                   help="generated negative queries (odd keys)")
-    p.add_argument("--neg-seed", type=int, default=0xFEEDBEEF)
-    p.add_argument("--threads", type=int, default=1, help="accepted; lookups run on the GPU")
-    _add_key_input(p, required=False)
-    p.set_defaults(func=cmd_fpr, keys=None)
-
-    p = sub.add_parser("hist", help="per-block load histogram of a filter")
-    p.add_argument("--filter", required=True)
-    p.set_defaults(func=cmd_hist)
+    for name, (help_text, options, defaults) in _COMMANDS.items():
+        p = sub.add_parser(name, help=help_text)
+        for opt in options:
+            if isinstance(opt, str):  # the key-stream group
+                for flag, kw in _KEY_INPUT:
+                    kw = dict(kw, required=True) if flag == "--keys" and opt == "@keys" else kw
+                    p.add_argument(flag, **kw)
+            else:
+                p.add_argument(opt[0], **opt[1])
+        p.set_defaults(func=_HANDLERS[name], **defaults)
     return parser
 
 

@@ -98,9 +98,10 @@ def test_relaxed_build_tolerance(golden, name):
     neg = probes[case["hits_pos"]:]
     hits = f.count_hits(neg)
     ref = case["hits_neg"]
-    # false positives within 10% (|log2 FPR ratio| <~ 0.14) plus 3 sigma of the
-    # Poisson noise of both counts (relaxed builds are timing-dependent)
-    assert abs(hits - ref) <= 0.1 * ref + 3 * np.sqrt(2.0 * max(ref, 1)) + 1
+    # false positives within 10% (|log2 FPR ratio| <~ 0.14) plus 4 sigma of the
+    # Poisson noise of both counts (relaxed builds are timing-dependent; 4
+    # sigma keeps the eight cases from flaking together)
+    assert abs(hits - ref) <= 0.1 * ref + 4 * np.sqrt(2.0 * max(ref, 1)) + 1
     hist = bb.block_load_histogram(f)
     assert abs(hist.mean_load - case["mean_load"]) <= max(1.0, 0.01 * case["mean_load"])
     assert abs(hist.variance / case["variance"] - 1) <= 0.15 + 0.3 * (f.num_blocks < 1000)
