@@ -124,23 +124,27 @@ BC_API int bc_contains_host(bc_filter *f, const uint64_t *d_words, const uint64_
 /* 2-bit canonical q-gram keys of a device byte sequence (io.py:158-177).
  * Windows touching any byte outside ACGTacgt are skipped, so several records
  * concatenated with a separator byte (e.g. '\n') never produce a window that
- * spans two records.  d_keys must hold len-q+1 keys; *d_count receives the
- * number written. */
+ * spans two records.  record_len > 0 declares the sequence to be consecutive
+ * records of record_len bytes with no separator (a reads matrix): windows that
+ * cross a record boundary are skipped too.  d_keys must hold len-q+1 keys;
+ * *d_count receives the number written. */
 BC_API int bc_encode_qgrams(const uint8_t *d_seq, uint64_t len, int q, int canonical,
-                     uint64_t *d_keys, unsigned long long *d_count, void *stream);
+                            uint64_t record_len, uint64_t *d_keys, unsigned long long *d_count,
+                            void *stream);
 
 /* Fused encode + insert: == bc_insert(f, words, encode_qgrams(seq), mode).
  * *d_count (nullable) receives the number of keys (valid windows) inserted. */
 BC_API int bc_insert_qgrams(bc_filter *f, uint64_t *d_words, const uint8_t *d_seq, uint64_t len,
-                     int q, int canonical, int mode, unsigned long long *d_count,
-                     void *stream);
+                            int q, int canonical, uint64_t record_len, int mode,
+                            unsigned long long *d_count, void *stream);
 
 /* Fused encode + lookup: == bc_contains(f, words, encode_qgrams(seq)).
  * d_out (nullable) must hold len-q+1 bytes; *d_count (nullable) receives the
  * number of valid windows (= number of answers written). */
 BC_API int bc_contains_qgrams(bc_filter *f, const uint64_t *d_words, const uint8_t *d_seq,
-                       uint64_t len, int q, int canonical, uint8_t *d_out,
-                       unsigned long long *d_count, unsigned long long *d_hits, void *stream);
+                              uint64_t len, int q, int canonical, uint64_t record_len,
+                              uint8_t *d_out, unsigned long long *d_count,
+                              unsigned long long *d_hits, void *stream);
 
 /* counts[j] += number of blocks holding j set bits, j in [0, block_bits]. */
 BC_API int bc_block_histogram(const uint64_t *d_words, uint64_t num_blocks, int block_bits,

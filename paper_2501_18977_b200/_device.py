@@ -67,9 +67,31 @@ def host_u64(x) -> np.ndarray:
     return np.ascontiguousarray(x, dtype=np.uint64)
 
 
+def sequence_records(seq, record_len=None) -> tuple:
+    """(sequence, record length): a 2-D byte array (reads x length) is a
+    matrix of fixed-length records -- flattened, with record_len its row
+    length; anything else is one sequence (record_len as given, 0 = none)."""
+    foreign = _foreign_cuda(seq)
+    if foreign is not None:
+        seq = foreign
+    if isinstance(seq, (torch.Tensor, np.ndarray)) and seq.ndim == 2:
+        rows, cols = seq.shape
+        if record_len not in (None, cols):
+            raise ValueError(f"record_len {record_len} does not match the row length {cols}")
+        return seq.reshape(rows * cols), int(cols)
+    return seq, int(record_len or 0)
+
+
 def as_device_bytes(seq, device: torch.device) -> torch.Tensor:
+    foreign = _foreign_cuda(seq)
+    if foreign is not None:
+        seq = foreign
     if isinstance(seq, torch.Tensor):
         return seq.to(device=device, dtype=torch.uint8).contiguous()
+    if isinstance(seq, np.ndarray):
+        raw = np.ascontiguousarray(seq, dtype=np.uint8).reshape(-1)
+        return torch.from_numpy(raw).to(device) if raw.size else \
+            torch.empty(0, dtype=torch.uint8, device=device)
     if isinstance(seq, str):
         seq = seq.encode("ascii", errors="replace")
     raw = np.frombuffer(bytes(seq), dtype=np.uint8)
@@ -99,16 +121,18 @@ def histogram(d_words: torch.Tensor, num_blocks: int, block_bits: int) -> np.nda
     return counts.cpu().numpy()
 
 
-def encode_qgrams(seq, q: int, canonical: bool):
-    """Device q-gram encoder; returns numpy (or a CUDA tensor for tensor input)."""
+def encode_qgrams(seq, q: int, canonical: bool, record_len=None):
+    """Device q-gram encoder; returns numpy (or a CUDA tensor for device input).
+    A 2-D input is a matrix of fixed-length records (no window crosses rows)."""
     dev = require_cuda()
     on_device = is_device_tensor(seq)
+    seq, rec = sequence_records(seq, record_len)
     d_seq = as_device_bytes(seq, dev)
     n = d_seq.numel()
     nwin = n - q + 1 if n >= q else 0
     keys = torch.empty(max(nwin, 1), dtype=torch.uint64, device=dev)
     cnt = torch.zeros(1, dtype=torch.int64, device=dev)
-    check(lib().bc_encode_qgrams(ptr(d_seq) if n else None, n, q, int(bool(canonical)),
+    check(lib().bc_encode_qgrams(ptr(d_seq) if n else None, n, q, int(bool(canonical)), rec,
                                  ptr(keys), ptr(cnt), stream_ptr(dev)))
     m = int(cnt.item())
     out = keys[:m]

@@ -81,9 +81,9 @@ def lib() -> ctypes.CDLL:
         L.bc_contains.argtypes = [P, P, P, u64, P, P, P]
         L.bc_insert_host.argtypes = [P, P, P, u64, ci, P]
         L.bc_contains_host.argtypes = [P, P, P, u64, P, P, P]
-        L.bc_encode_qgrams.argtypes = [P, u64, ci, ci, P, P, P]
-        L.bc_insert_qgrams.argtypes = [P, P, P, u64, ci, ci, ci, P, P]
-        L.bc_contains_qgrams.argtypes = [P, P, P, u64, ci, ci, P, P, P, P]
+        L.bc_encode_qgrams.argtypes = [P, u64, ci, ci, u64, P, P, P]
+        L.bc_insert_qgrams.argtypes = [P, P, P, u64, ci, ci, u64, ci, P, P]
+        L.bc_contains_qgrams.argtypes = [P, P, P, u64, ci, ci, u64, P, P, P, P]
         L.bc_block_histogram.argtypes = [P, u64, ci, P, P]
         L.bc_route.argtypes = [P, P, u64, P, P]
         L.bc_eval_hash.argtypes = [u64, u64, P, u64, P, P]

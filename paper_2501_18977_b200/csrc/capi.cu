@@ -397,7 +397,8 @@ extern "C" int bc_contains(bc_filter *f, const uint64_t *d_words, const uint64_t
 static u64 qgram_windows(u64 len, int q) { return len >= (u64)q ? len - (u64)q + 1 : 0; }
 
 extern "C" int bc_encode_qgrams(const uint8_t *d_seq, uint64_t len, int q, int canonical,
-                                uint64_t *d_keys, unsigned long long *d_count, void *stream) {
+                                uint64_t record_len, uint64_t *d_keys,
+                                unsigned long long *d_count, void *stream) {
     if (q < 1 || q > 32) return fail(BC_EINVAL, "q must be in [1, 32], got %d", q);
     cudaStream_t s = (cudaStream_t)stream;
     const u64 nwin = qgram_windows(len, q);
@@ -409,8 +410,9 @@ extern "C" int bc_encode_qgrams(const uint8_t *d_seq, uint64_t len, int q, int c
     const u64 ntiles = (nwin + kQgramTile - 1) / kQgramTile;
     u64 *tiles = nullptr;
     CUDA_TRY(cudaMallocAsync((void **)&tiles, sizeof(u64) * ntiles, s));
-    cudaError_t e = launch_qgram_offsets(d_seq, len, q, tiles, ntiles, d_count, s);
-    if (e == cudaSuccess) e = launch_qgram_encode(d_seq, len, q, canonical, tiles, d_keys, s);
+    const RecSpec rec{record_len, 0};
+    cudaError_t e = launch_qgram_offsets(d_seq, len, q, rec, tiles, ntiles, d_count, s);
+    if (e == cudaSuccess) e = launch_qgram_encode(d_seq, len, q, canonical, rec, tiles, d_keys, s);
     cudaFreeAsync(tiles, s);
     CUDA_TRY(e);
     return BC_OK;
@@ -418,8 +420,8 @@ extern "C" int bc_encode_qgrams(const uint8_t *d_seq, uint64_t len, int q, int c
 
 // Materialise the keys (for the paths the fused kernel does not cover:
 // ordered c >= 2 inserts, standard filters, non-512-bit blocks).
-static int encode_tmp(const u8 *seq, u64 len, int q, int canonical, u64 **keys, u64 *n,
-                      cudaStream_t s) {
+static int encode_tmp(const u8 *seq, u64 len, int q, int canonical, u64 rec, u64 **keys,
+                      u64 *n, cudaStream_t s) {
     const u64 nwin = qgram_windows(len, q);
     *keys = nullptr;
     *n = 0;
@@ -427,7 +429,7 @@ static int encode_tmp(const u8 *seq, u64 len, int q, int canonical, u64 **keys, 
     unsigned long long *d_cnt = nullptr;
     CUDA_TRY(cudaMallocAsync((void **)keys, sizeof(u64) * nwin, s));
     CUDA_TRY(cudaMallocAsync((void **)&d_cnt, sizeof(*d_cnt), s));
-    int rc = bc_encode_qgrams(seq, len, q, canonical, *keys, d_cnt, s);
+    int rc = bc_encode_qgrams(seq, len, q, canonical, rec, *keys, d_cnt, s);
     unsigned long long h_cnt = 0;
     if (rc == BC_OK) {
         cudaError_t e = cudaMemcpyAsync(&h_cnt, d_cnt, sizeof h_cnt, cudaMemcpyDeviceToHost, s);
@@ -440,8 +442,8 @@ static int encode_tmp(const u8 *seq, u64 len, int q, int canonical, u64 **keys, 
 }
 
 extern "C" int bc_insert_qgrams(bc_filter *f, uint64_t *d_words, const uint8_t *d_seq,
-                                uint64_t len, int q, int canonical, int mode,
-                                unsigned long long *d_count, void *stream) {
+                                uint64_t len, int q, int canonical, uint64_t record_len,
+                                int mode, unsigned long long *d_count, void *stream) {
     if (!f) return fail(BC_EINVAL, "null filter");
     if (q < 1 || q > 32) return fail(BC_EINVAL, "q must be in [1, 32], got %d", q);
     if (mode != BC_INSERT_ORDERED && mode != BC_INSERT_RELAXED)
@@ -459,13 +461,14 @@ extern "C" int bc_insert_qgrams(bc_filter *f, uint64_t *d_words, const uint8_t *
         const u64 per = f->kp.c == 1 ? nwin : std::max<u64>(1, f->kp.num_blocks / 2);
         for (u64 w = 0; w < nwin; w += per) {
             const u64 nw = std::min(per, nwin - w);
+            const RecSpec rec{record_len, record_len ? w % record_len : 0};
             CUDA_TRY(launch_qgram_blocks(OP_INSERT, f->kp, d_words, d_seq + w, nw + q - 1, q,
-                                         canonical, nullptr, nullptr, nullptr, d_count, s));
+                                         canonical, rec, nullptr, nullptr, nullptr, d_count, s));
         }
         return BC_OK;
     }
     u64 *keys = nullptr, n = 0;
-    int rc = encode_tmp(d_seq, len, q, canonical, &keys, &n, s);
+    int rc = encode_tmp(d_seq, len, q, canonical, record_len, &keys, &n, s);
     if (rc == BC_OK) rc = insert_device(f, d_words, keys, n, mode, s);
     if (rc == BC_OK && d_count) {
         unsigned long long hn = n;
@@ -478,9 +481,9 @@ extern "C" int bc_insert_qgrams(bc_filter *f, uint64_t *d_words, const uint8_t *
 }
 
 extern "C" int bc_contains_qgrams(bc_filter *f, const uint64_t *d_words, const uint8_t *d_seq,
-                                  uint64_t len, int q, int canonical, uint8_t *d_out,
-                                  unsigned long long *d_count, unsigned long long *d_hits,
-                                  void *stream) {
+                                  uint64_t len, int q, int canonical, uint64_t record_len,
+                                  uint8_t *d_out, unsigned long long *d_count,
+                                  unsigned long long *d_hits, void *stream) {
     if (!f) return fail(BC_EINVAL, "null filter");
     if (q < 1 || q > 32) return fail(BC_EINVAL, "q must be in [1, 32], got %d", q);
     if (int rc = check_device(f)) return rc;
@@ -497,20 +500,22 @@ extern "C" int bc_contains_qgrams(bc_filter *f, const uint64_t *d_words, const u
         const bool need_off = d_out != nullptr || d_count != nullptr;
         if (need_off) {
             CUDA_TRY(cudaMallocAsync((void **)&tiles, sizeof(u64) * ntiles, s));
-            cudaError_t e = launch_qgram_offsets(d_seq, len, q, tiles, ntiles, d_count, s);
+            cudaError_t e = launch_qgram_offsets(d_seq, len, q, RecSpec{record_len, 0}, tiles,
+                                                 ntiles, d_count, s);
             if (e != cudaSuccess) {
                 cudaFreeAsync(tiles, s);
                 CUDA_TRY(e);
             }
         }
         cudaError_t e = launch_qgram_blocks(OP_CONTAINS, f->kp, const_cast<u64 *>(d_words), d_seq,
-                                            len, q, canonical, tiles, d_out, d_hits, nullptr, s);
+                                            len, q, canonical, RecSpec{record_len, 0}, tiles,
+                                            d_out, d_hits, nullptr, s);
         if (tiles) cudaFreeAsync(tiles, s);
         CUDA_TRY(e);
         return BC_OK;
     }
     u64 *keys = nullptr, n = 0;
-    int rc = encode_tmp(d_seq, len, q, canonical, &keys, &n, s);
+    int rc = encode_tmp(d_seq, len, q, canonical, record_len, &keys, &n, s);
     if (rc == BC_OK) rc = contains_device(f, d_words, keys, n, d_out, d_hits, s);
     if (rc == BC_OK && d_count) {
         unsigned long long hn = n;

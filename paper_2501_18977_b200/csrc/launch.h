@@ -47,14 +47,20 @@ cudaError_t launch_eval_hash(DevHash h, const u64 *keys, u64 n, u64 *out, cudaSt
 constexpr int kQgramThreads = 256;
 constexpr int kQgramPerThread = 8;
 constexpr int kQgramTile = kQgramThreads * kQgramPerThread;
-cudaError_t launch_qgram_offsets(const u8 *seq, u64 len, int q, u64 *tile_off, u64 ntiles,
-                                 unsigned long long *total, cudaStream_t s);
-cudaError_t launch_qgram_encode(const u8 *seq, u64 len, int q, int canonical,
+// Records of a q-gram sequence: len > 0 means consecutive records of len
+// bytes (windows never cross them), phase = offset of seq[0] in its record.
+struct RecSpec {
+    u64 len = 0;
+    u64 phase = 0;
+};
+cudaError_t launch_qgram_offsets(const u8 *seq, u64 len, int q, RecSpec rec, u64 *tile_off,
+                                 u64 ntiles, unsigned long long *total, cudaStream_t s);
+cudaError_t launch_qgram_encode(const u8 *seq, u64 len, int q, int canonical, RecSpec rec,
                                 const u64 *tile_off, u64 *keys, cudaStream_t s);
 // Fused: encode + (insert | contains).  tile_off may be NULL when no ordered
 // output is needed (inserts, count-only lookups).
 cudaError_t launch_qgram_blocks(int op, const KParams &p, u64 *words, const u8 *seq, u64 len,
-                                int q, int canonical, const u64 *tile_off, u8 *out,
+                                int q, int canonical, RecSpec rec, const u64 *tile_off, u8 *out,
                                 unsigned long long *hits, unsigned long long *count,
                                 cudaStream_t s);
 

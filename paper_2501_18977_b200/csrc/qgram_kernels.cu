@@ -43,8 +43,23 @@ struct Roller {
 
 // Stage, roll and compact one tile; returns the number of valid windows,
 // whose keys are left in order in sm.keys[0..V).
+// With records (rec.len > 0) a window is also invalid when it crosses a record
+// boundary.
+__device__ __forceinline__ u32 in_record_mask(u64 wfirst, int q, RecSpec rec) {
+    if (rec.len == 0) return (1u << kQgramPerThread) - 1u;
+    u64 r = (wfirst + rec.phase) % rec.len;
+    u32 m = 0;
+#pragma unroll
+    for (int k = 0; k < kQgramPerThread; ++k) {
+        m |= (r + (u64)q <= rec.len ? 1u : 0u) << k;
+        r = r + 1 == rec.len ? 0 : r + 1;
+    }
+    return m;
+}
+
 __device__ __forceinline__ u32 tile_encode(const u8 *__restrict__ seq, u64 len, int q,
-                                           int canonical, u64 w0, u64 nwin, QgramSmem &sm) {
+                                           int canonical, RecSpec rec, u64 w0, u64 nwin,
+                                           QgramSmem &sm) {
     const int tid = threadIdx.x;
     const u64 nbytes_avail = len - w0;  // w0 < nwin <= len
     const int nbytes = kQgramTile + q - 1;
@@ -65,6 +80,7 @@ __device__ __forceinline__ u32 tile_encode(const u8 *__restrict__ seq, u64 len, 
         code[k] = (canonical && r.rc < r.fw) ? r.rc : r.fw;
         vmask |= (v ? 1u : 0u) << k;
     }
+    vmask &= in_record_mask(wfirst, q, rec);
     // CTA exclusive scan of the per-thread valid counts
     const u32 mine = __popc(vmask);
     u32 incl = mine;
@@ -92,8 +108,8 @@ __device__ __forceinline__ u32 tile_encode(const u8 *__restrict__ seq, u64 len, 
 }
 
 __global__ void __launch_bounds__(kQgramThreads) qgram_count_kernel(const u8 *__restrict__ seq,
-                                                                    u64 len, int q, u64 nwin,
-                                                                    u64 ntiles,
+                                                                    u64 len, int q, RecSpec rec,
+                                                                    u64 nwin, u64 ntiles,
                                                                     u64 *__restrict__ counts) {
     __shared__ u8 bytes[kQgramTile + 32];
     __shared__ u32 warp_tot[kQgramThreads / 32];
@@ -107,13 +123,14 @@ __global__ void __launch_bounds__(kQgramThreads) qgram_count_kernel(const u8 *__
         Roller r(q);
         const u8 *b = bytes + kQgramPerThread * tid;
         for (int j = 0; j < q - 1; ++j) r.step(b[j]);
-        u32 mine = 0;
+        u32 vmask = 0;
         const u64 wfirst = w0 + (u64)kQgramPerThread * tid;
 #pragma unroll
         for (int k = 0; k < kQgramPerThread; ++k) {
             r.step(b[q - 1 + k]);
-            mine += (r.run >= (u32)q && wfirst + k < nwin) ? 1u : 0u;
+            vmask |= ((r.run >= (u32)q && wfirst + k < nwin) ? 1u : 0u) << k;
         }
+        u32 mine = __popc(vmask & in_record_mask(wfirst, q, rec));
         for (int o = 16; o > 0; o >>= 1) mine += __shfl_xor_sync(kFull, mine, o);
         if ((tid & 31) == 0) warp_tot[tid >> 5] = mine;
         __syncthreads();
@@ -159,11 +176,11 @@ __global__ void __launch_bounds__(1024) scan_kernel(u64 *__restrict__ v, u64 n,
 }
 
 __global__ void __launch_bounds__(kQgramThreads) qgram_encode_kernel(
-    const u8 *__restrict__ seq, u64 len, int q, int canonical, u64 nwin, u64 ntiles,
+    const u8 *__restrict__ seq, u64 len, int q, int canonical, RecSpec rec, u64 nwin, u64 ntiles,
     const u64 *__restrict__ tile_off, u64 *__restrict__ keys) {
     __shared__ QgramSmem sm;
     for (u64 tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        const u32 v = tile_encode(seq, len, q, canonical, tile * kQgramTile, nwin, sm);
+        const u32 v = tile_encode(seq, len, q, canonical, rec, tile * kQgramTile, nwin, sm);
         const u64 base = tile_off[tile];
         for (u32 i = threadIdx.x; i < v; i += kQgramThreads) keys[base + i] = sm.keys[i];
         __syncthreads();
@@ -173,8 +190,8 @@ __global__ void __launch_bounds__(kQgramThreads) qgram_encode_kernel(
 template <int OP, int C>
 __global__ void __launch_bounds__(kQgramThreads) qgram_blocks_kernel(
     const __grid_constant__ KParams p, u64 *__restrict__ words, const u8 *__restrict__ seq,
-    u64 len, int q, int canonical, u64 nwin, u64 ntiles, const u64 *__restrict__ tile_off,
-    u8 *__restrict__ out, unsigned long long *__restrict__ hits,
+    u64 len, int q, int canonical, RecSpec rec, u64 nwin, u64 ntiles,
+    const u64 *__restrict__ tile_off, u8 *__restrict__ out, unsigned long long *__restrict__ hits,
     unsigned long long *__restrict__ count) {
     static_assert(kQgramThreads == kTPB, "tile pipeline assumes the CTA shape of blocks.cuh");
     __shared__ QgramSmem qs;
@@ -183,7 +200,7 @@ __global__ void __launch_bounds__(kQgramThreads) qgram_blocks_kernel(
     WarpSmem<C> &ws = smem[warp];
     u32 my_hits = 0;
     for (u64 tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        const u32 v = tile_encode(seq, len, q, canonical, tile * kQgramTile, nwin, qs);
+        const u32 v = tile_encode(seq, len, q, canonical, rec, tile * kQgramTile, nwin, qs);
         const u64 obase = (OP == OP_CONTAINS && tile_off) ? tile_off[tile] : 0ull;
         if (count != nullptr && tid == 0 && v) atomicAdd(count, (unsigned long long)v);
         // each warp takes 32 consecutive compacted keys at a time
@@ -209,15 +226,15 @@ __global__ void __launch_bounds__(kQgramThreads) qgram_blocks_kernel(
 template <int C>
 __global__ void __launch_bounds__(kQgramThreads) qgram_lookup_kernel(
     const __grid_constant__ KParams p, const u64 *__restrict__ words, const u8 *__restrict__ seq,
-    u64 len, int q, int canonical, u64 nwin, u64 ntiles, const u64 *__restrict__ tile_off,
-    u8 *__restrict__ out, unsigned long long *__restrict__ hits) {
+    u64 len, int q, int canonical, RecSpec rec, u64 nwin, u64 ntiles,
+    const u64 *__restrict__ tile_off, u8 *__restrict__ out, unsigned long long *__restrict__ hits) {
     __shared__ QgramSmem qs;
     __shared__ LookupSmem<C> smem[kWarps];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     LookupSmem<C> &ls = smem[warp];
     u32 my_hits = 0;
     for (u64 tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        const u32 v = tile_encode(seq, len, q, canonical, tile * kQgramTile, nwin, qs);
+        const u32 v = tile_encode(seq, len, q, canonical, rec, tile * kQgramTile, nwin, qs);
         const u64 obase = tile_off ? tile_off[tile] : 0ull;
         for (u32 sub = 32u * warp; sub < v; sub += 32u * kWarps) {
             const bool valid = sub + lane < v;
@@ -244,35 +261,35 @@ cudaError_t launch_scan(u64 *v, u64 n, unsigned long long *total, cudaStream_t s
 // ---------------------------------------------------------------------------------
 static inline u64 n_windows(u64 len, int q) { return len >= (u64)q ? len - q + 1 : 0; }
 
-cudaError_t launch_qgram_offsets(const u8 *seq, u64 len, int q, u64 *tile_off, u64 ntiles,
-                                 unsigned long long *total, cudaStream_t s) {
+cudaError_t launch_qgram_offsets(const u8 *seq, u64 len, int q, RecSpec rec, u64 *tile_off,
+                                 u64 ntiles, unsigned long long *total, cudaStream_t s) {
     const u64 nwin = n_windows(len, q);
     if (nwin == 0) {
         if (total) return cudaMemsetAsync(total, 0, sizeof(*total), s);
         return cudaSuccess;
     }
     const unsigned grid = grid_for((const void *)qgram_count_kernel, kQgramThreads, 0, ntiles);
-    qgram_count_kernel<<<grid, kQgramThreads, 0, s>>>(seq, len, q, nwin, ntiles, tile_off);
+    qgram_count_kernel<<<grid, kQgramThreads, 0, s>>>(seq, len, q, rec, nwin, ntiles, tile_off);
     scan_kernel<<<1, 1024, 0, s>>>(tile_off, ntiles, total);
     count_launch(2);
     return cudaGetLastError();
 }
 
-cudaError_t launch_qgram_encode(const u8 *seq, u64 len, int q, int canonical,
+cudaError_t launch_qgram_encode(const u8 *seq, u64 len, int q, int canonical, RecSpec rec,
                                 const u64 *tile_off, u64 *keys, cudaStream_t s) {
     const u64 nwin = n_windows(len, q);
     if (nwin == 0) return cudaSuccess;
     const u64 ntiles = (nwin + kQgramTile - 1) / kQgramTile;
     const unsigned grid = grid_for((const void *)qgram_encode_kernel, kQgramThreads, 0, ntiles);
-    qgram_encode_kernel<<<grid, kQgramThreads, 0, s>>>(seq, len, q, canonical, nwin, ntiles,
-                                                       tile_off, keys);
+    qgram_encode_kernel<<<grid, kQgramThreads, 0, s>>>(seq, len, q, canonical, rec, nwin,
+                                                       ntiles, tile_off, keys);
     count_launch();
     return cudaGetLastError();
 }
 
 template <int OP, int C>
 static cudaError_t launch_qb(const KParams &p, u64 *words, const u8 *seq, u64 len, int q,
-                             int canonical, const u64 *tile_off, u8 *out,
+                             int canonical, RecSpec rec, const u64 *tile_off, u8 *out,
                              unsigned long long *hits, unsigned long long *count,
                              cudaStream_t s) {
     const u64 nwin = n_windows(len, q);
@@ -282,46 +299,46 @@ static cudaError_t launch_qb(const KParams &p, u64 *words, const u8 *seq, u64 le
         const void *fl = (const void *)qgram_lookup_kernel<C>;
         const unsigned g = grid_for(fl, kQgramThreads, 0, ntiles);
         qgram_lookup_kernel<C><<<g, kQgramThreads, 0, s>>>(p, words, seq, len, q, canonical,
-                                                           nwin, ntiles, tile_off, out, hits);
+                                                           rec, nwin, ntiles, tile_off, out, hits);
         count_launch();
         return cudaGetLastError();
     }
     const void *fn = (const void *)qgram_blocks_kernel<OP, C>;
     const unsigned grid = grid_for(fn, kQgramThreads, 0, ntiles);
     qgram_blocks_kernel<OP, C><<<grid, kQgramThreads, 0, s>>>(p, words, seq, len, q, canonical,
-                                                               nwin, ntiles, tile_off, out, hits,
-                                                               count);
+                                                               rec, nwin, ntiles, tile_off, out,
+                                                               hits, count);
     count_launch();
     return cudaGetLastError();
 }
 
 template <int OP>
 static cudaError_t launch_qb_c(const KParams &p, u64 *words, const u8 *seq, u64 len, int q,
-                               int canonical, const u64 *tile_off, u8 *out,
+                               int canonical, RecSpec rec, const u64 *tile_off, u8 *out,
                                unsigned long long *hits, unsigned long long *count,
                                cudaStream_t s) {
     switch (p.c) {
-        case 1: return launch_qb<OP, 1>(p, words, seq, len, q, canonical, tile_off, out, hits, count, s);
-        case 2: return launch_qb<OP, 2>(p, words, seq, len, q, canonical, tile_off, out, hits, count, s);
-        case 3: return launch_qb<OP, 3>(p, words, seq, len, q, canonical, tile_off, out, hits, count, s);
-        case 4: return launch_qb<OP, 4>(p, words, seq, len, q, canonical, tile_off, out, hits, count, s);
-        case 5: return launch_qb<OP, 5>(p, words, seq, len, q, canonical, tile_off, out, hits, count, s);
-        case 6: return launch_qb<OP, 6>(p, words, seq, len, q, canonical, tile_off, out, hits, count, s);
-        case 7: return launch_qb<OP, 7>(p, words, seq, len, q, canonical, tile_off, out, hits, count, s);
-        case 8: return launch_qb<OP, 8>(p, words, seq, len, q, canonical, tile_off, out, hits, count, s);
+        case 1: return launch_qb<OP, 1>(p, words, seq, len, q, canonical, rec, tile_off, out, hits, count, s);
+        case 2: return launch_qb<OP, 2>(p, words, seq, len, q, canonical, rec, tile_off, out, hits, count, s);
+        case 3: return launch_qb<OP, 3>(p, words, seq, len, q, canonical, rec, tile_off, out, hits, count, s);
+        case 4: return launch_qb<OP, 4>(p, words, seq, len, q, canonical, rec, tile_off, out, hits, count, s);
+        case 5: return launch_qb<OP, 5>(p, words, seq, len, q, canonical, rec, tile_off, out, hits, count, s);
+        case 6: return launch_qb<OP, 6>(p, words, seq, len, q, canonical, rec, tile_off, out, hits, count, s);
+        case 7: return launch_qb<OP, 7>(p, words, seq, len, q, canonical, rec, tile_off, out, hits, count, s);
+        case 8: return launch_qb<OP, 8>(p, words, seq, len, q, canonical, rec, tile_off, out, hits, count, s);
     }
     return cudaErrorInvalidValue;
 }
 
 cudaError_t launch_qgram_blocks(int op, const KParams &p, u64 *words, const u8 *seq, u64 len,
-                                int q, int canonical, const u64 *tile_off, u8 *out,
+                                int q, int canonical, RecSpec rec, const u64 *tile_off, u8 *out,
                                 unsigned long long *hits, unsigned long long *count,
                                 cudaStream_t s) {
     if (p.wpb != 8) return cudaErrorInvalidValue;  // caller falls back to encode + array path
     l2_release();
-    return op == OP_CONTAINS ? launch_qb_c<OP_CONTAINS>(p, words, seq, len, q, canonical,
+    return op == OP_CONTAINS ? launch_qb_c<OP_CONTAINS>(p, words, seq, len, q, canonical, rec,
                                                         tile_off, out, hits, count, s)
-                             : launch_qb_c<OP_INSERT>(p, words, seq, len, q, canonical,
+                             : launch_qb_c<OP_INSERT>(p, words, seq, len, q, canonical, rec,
                                                       tile_off, out, hits, count, s);
 }
 

@@ -446,56 +446,62 @@ class Filter:
             return int(hits.value)
 
     # -- fused DNA q-gram path ------------------------------------------------------------------
-    def insert_qgrams(self, enc, sequence, mode: str | None = None) -> int:
+    def insert_qgrams(self, enc, sequence, mode: str | None = None,
+                      record_len: int | None = None) -> int:
         """== insert_many(encode_qgrams(enc, sequence)); returns the number of
-        keys inserted.  The key array is never materialised."""
-        from ._device import as_device_bytes, ptr, stream_ptr
+        keys inserted.  The key array is never materialised.  A 2-D byte array
+        (reads x length), or ``record_len``, marks fixed-length records that
+        no window may cross."""
+        from ._device import as_device_bytes, ptr, sequence_records, stream_ptr
 
         m = self._mode(mode)
         dev = self.device
         with torch.cuda.device(dev):
-            seq = as_device_bytes(sequence, dev)
+            flat, rec = sequence_records(sequence, record_len)
+            seq = as_device_bytes(flat, dev)
             n = seq.numel()
             d_cnt = torch.zeros(1, dtype=torch.int64, device=dev)
             check(lib().bc_insert_qgrams(self.handle, ptr(self.storage.d_words),
                                          ptr(seq) if n else None, n, enc.q,
-                                         int(enc.canonical), m, ptr(d_cnt), stream_ptr(dev)))
+                                         int(enc.canonical), rec, m, ptr(d_cnt),
+                                         stream_ptr(dev)))
             cnt = int(d_cnt.item())
         self.storage.device_modified()
         self.inserted += cnt
         return cnt
 
-    def contains_qgrams(self, enc, sequence):
-        """== contains_many(encode_qgrams(enc, sequence))."""
-        from ._device import as_device_bytes, is_device_tensor, ptr, stream_ptr
+    def _qgram_lookup(self, enc, sequence, record_len, want_answers: bool):
+        from ._device import as_device_bytes, ptr, sequence_records, stream_ptr
 
         dev = self.device
         with torch.cuda.device(dev):
-            seq = as_device_bytes(sequence, dev)
+            flat, rec = sequence_records(sequence, record_len)
+            seq = as_device_bytes(flat, dev)
             n = seq.numel()
-            nwin = max(0, n - enc.q + 1)
-            out = torch.empty(max(nwin, 1), dtype=torch.uint8, device=dev)
-            cnt = torch.zeros(1, dtype=torch.int64, device=dev)
+            out = cnt = hits = None
+            if want_answers:
+                out = torch.empty(max(n - enc.q + 1, 1), dtype=torch.uint8, device=dev)
+                cnt = torch.zeros(1, dtype=torch.int64, device=dev)
+            else:
+                hits = torch.zeros(1, dtype=torch.int64, device=dev)
             check(lib().bc_contains_qgrams(self.handle, ptr(self.storage.d_words),
                                            ptr(seq) if n else None, n, enc.q,
-                                           int(enc.canonical), ptr(out), ptr(cnt), None,
-                                           stream_ptr(dev)))
-            res = out[:int(cnt.item())].view(torch.bool)
+                                           int(enc.canonical), rec, ptr(out), ptr(cnt),
+                                           ptr(hits), stream_ptr(dev)))
+            if want_answers:
+                return out[:int(cnt.item())].view(torch.bool)
+            return int(hits.item())
+
+    def contains_qgrams(self, enc, sequence, record_len: int | None = None):
+        """== contains_many(encode_qgrams(enc, sequence)); records as in
+        ``insert_qgrams``."""
+        from ._device import is_device_tensor
+
+        res = self._qgram_lookup(enc, sequence, record_len, True)
         return res if is_device_tensor(sequence) else res.cpu().numpy()
 
-    def count_qgram_hits(self, enc, sequence) -> int:
-        from ._device import as_device_bytes, ptr, stream_ptr
-
-        dev = self.device
-        with torch.cuda.device(dev):
-            seq = as_device_bytes(sequence, dev)
-            n = seq.numel()
-            hits = torch.zeros(1, dtype=torch.int64, device=dev)
-            check(lib().bc_contains_qgrams(self.handle, ptr(self.storage.d_words),
-                                           ptr(seq) if n else None, n, enc.q,
-                                           int(enc.canonical), None, None, ptr(hits),
-                                           stream_ptr(dev)))
-            return int(hits.item())
+    def count_qgram_hits(self, enc, sequence, record_len: int | None = None) -> int:
+        return self._qgram_lookup(enc, sequence, record_len, False)
 
     def route_many(self, keys):
         """Shard index per key (GPU)."""

@@ -29,11 +29,13 @@ class QGramEncoder:
             raise ValueError(f"q must be in [1, 32], got {self.q}")
 
 
-def encode_qgrams(enc: QGramEncoder, sequence):
-    """All valid q-gram keys of a sequence, in sequence order (GPU)."""
+def encode_qgrams(enc: QGramEncoder, sequence, record_len: int | None = None):
+    """All valid q-gram keys of a sequence, in sequence order (GPU).  A 2-D
+    byte array (reads x length), or ``record_len``, marks fixed-length records
+    that no window may cross."""
     from ._device import encode_qgrams as _enc
 
-    return _enc(sequence, enc.q, enc.canonical)
+    return _enc(sequence, enc.q, enc.canonical, record_len)
 
 
 def join_records(records, sep: bytes = b"\n") -> bytes:

@@ -589,3 +589,45 @@ def test_foreign_cuda_arrays_stay_on_device(golden):
         assert isinstance(out, torch.Tensor) and out.is_cuda
         assert sha(out.cpu().numpy().astype(np.uint8)) == case["out_sha256"]
         assert f.count_hits(wrap(t_probes)) == case["hits_pos"] + case["hits_neg"]
+
+
+@pytest.mark.parametrize("canonical", [True, False])
+def test_qgram_read_matrix_records(canonical):
+    """A 2-D reads matrix (fixed-length records, no separators): encode,
+    fused insert and fused lookup equal the per-read composition through the
+    oracle; no window crosses a row (also with the relaxed insert's slicing,
+    whose slices start mid-record)."""
+    rng = np.random.default_rng(12)
+    reads = rng.choice(np.frombuffer(b"ACGTacgtN", np.uint8), size=(397, 151),
+                       p=[0.124] * 8 + [0.008])
+    q = 31
+    enc = bb.QGramEncoder(q, canonical=canonical)
+    want = np.concatenate([orc.encode_qgrams(r.tobytes(), q, canonical) for r in reads])
+    got = bb.encode_qgrams(enc, reads)
+    np.testing.assert_array_equal(got, want)
+    got_t = bb.encode_qgrams(enc, torch.from_numpy(reads).cuda())
+    assert got_t.is_cuda
+    np.testing.assert_array_equal(got_t.cpu().numpy(), want)
+    np.testing.assert_array_equal(bb.encode_qgrams(enc, reads.reshape(-1), record_len=151),
+                                  want)
+
+    for kind, c, mode in (("blocked", 1, "ordered"), ("blowchoc", 2, "ordered"),
+                          ("blowchoc", 2, "relaxed")):
+        cfg = bb.FilterConfig(kind=kind, k=9, choices=c, n_capacity=3000, seed=4)
+        f = bb.Filter.from_config(cfg, insert_mode=mode)
+        assert f.insert_qgrams(enc, reads) == want.size
+        if mode == "ordered":
+            o = orc.make_filter(kind, k=9, choices=c, n_capacity=3000, seed=4)
+            o.insert_many(want)
+            np.testing.assert_array_equal(f.storage.words, o.words)
+        assert f.contains_many(want).all()
+        probe = rng.choice(np.frombuffer(b"ACGT", np.uint8), size=(50, 151))
+        pk = np.concatenate([want[:500]] + [orc.encode_qgrams(r.tobytes(), q, canonical)
+                                            for r in probe])
+        both = np.concatenate([reads[:5], probe])
+        pw = np.concatenate([orc.encode_qgrams(r.tobytes(), q, canonical) for r in both])
+        np.testing.assert_array_equal(f.contains_qgrams(enc, both), f.contains_many(pw))
+        assert f.count_qgram_hits(enc, both) == int(f.contains_many(pw).sum())
+        del pk
+    with pytest.raises(ValueError):
+        bb.encode_qgrams(enc, reads, record_len=150)

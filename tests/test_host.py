@@ -183,7 +183,7 @@ def test_abi_argument_errors_without_gpu():
     assert L.bc_contains(None, None, None, 0, None, None, None) == _native.BC_EINVAL
     assert b"null filter" in L.bc_last_error()
     assert L.bc_eval_hash(3, 0, None, 0, None, None) == _native.BC_EINVAL
-    assert L.bc_encode_qgrams(None, 10, 33, 1, None, None, None) == _native.BC_EINVAL
+    assert L.bc_encode_qgrams(None, 10, 33, 1, 0, None, None, None) == _native.BC_EINVAL
     assert L.bc_block_histogram(None, 1, 48, None, None) == _native.BC_EINVAL
     d = _native.BcFilterDesc()
     d.kind, d.k, d.choices, d.block_bits, d.num_blocks, d.shards = 2, 4, 9, 512, 8, 1
