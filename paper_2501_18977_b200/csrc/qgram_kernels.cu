@@ -223,7 +223,7 @@ __global__ void __launch_bounds__(kQgramThreads) qgram_blocks_kernel(
 
 // Lookups with the random strategy: the compacted keys go through the
 // staged-block tile with early exit over the choices (lookup.cuh).
-template <int C>
+template <int C, int K>
 __global__ void __launch_bounds__(kQgramThreads) qgram_lookup_kernel(
     const __grid_constant__ KParams p, const u64 *__restrict__ words, const u8 *__restrict__ seq,
     u64 len, int q, int canonical, RecSpec rec, u64 nwin, u64 ntiles,
@@ -238,8 +238,8 @@ __global__ void __launch_bounds__(kQgramThreads) qgram_lookup_kernel(
         const u64 obase = tile_off ? tile_off[tile] : 0ull;
         for (u32 sub = 32u * warp; sub < v; sub += 32u * kWarps) {
             const bool valid = sub + lane < v;
-            const bool f = lookup_tile<C>(p, words, ls, valid ? qs.keys[sub + lane] : 0ull,
-                                          valid, lane);
+            const bool f = lookup_tile<C, K>(p, words, ls, valid ? qs.keys[sub + lane] : 0ull,
+                                             valid, lane);
             if (out != nullptr && valid) out[obase + sub + lane] = (u8)f;
             my_hits += f ? 1u : 0u;
             __syncwarp();
@@ -287,6 +287,42 @@ cudaError_t launch_qgram_encode(const u8 *seq, u64 len, int q, int canonical, Re
     return cudaGetLastError();
 }
 
+template <int C, int K>
+static cudaError_t launch_qgram_lookup_k(const KParams &p, const u64 *words, const u8 *seq,
+                                         u64 len, int q, int canonical, RecSpec rec, u64 nwin,
+                                         u64 ntiles, const u64 *tile_off, u8 *out,
+                                         unsigned long long *hits, cudaStream_t s) {
+    const void *fl = (const void *)qgram_lookup_kernel<C, K>;
+    const unsigned g = grid_for(fl, kQgramThreads, 0, ntiles);
+    qgram_lookup_kernel<C, K><<<g, kQgramThreads, 0, s>>>(p, words, seq, len, q, canonical, rec,
+                                                          nwin, ntiles, tile_off, out, hits);
+    count_launch();
+    return cudaGetLastError();
+}
+
+// compile-time k (4..16) for one to three choices, as for key arrays
+template <int C>
+static cudaError_t launch_qgram_lookup(const KParams &p, const u64 *words, const u8 *seq,
+                                       u64 len, int q, int canonical, RecSpec rec, u64 nwin,
+                                       u64 ntiles, const u64 *tile_off, u8 *out,
+                                       unsigned long long *hits, cudaStream_t s) {
+    if (C <= 3) {
+        switch (p.k) {
+#define BC_QL_K(k)                                                                          \
+    case k:                                                                                 \
+        return launch_qgram_lookup_k<C, (C <= 3 ? k : 0)>(p, words, seq, len, q, canonical, \
+                                                          rec, nwin, ntiles, tile_off, out,  \
+                                                          hits, s);
+            BC_QL_K(4) BC_QL_K(5) BC_QL_K(6) BC_QL_K(7) BC_QL_K(8) BC_QL_K(9) BC_QL_K(10)
+            BC_QL_K(11) BC_QL_K(12) BC_QL_K(13) BC_QL_K(14) BC_QL_K(15) BC_QL_K(16)
+#undef BC_QL_K
+            default: break;
+        }
+    }
+    return launch_qgram_lookup_k<C, 0>(p, words, seq, len, q, canonical, rec, nwin, ntiles,
+                                       tile_off, out, hits, s);
+}
+
 template <int OP, int C>
 static cudaError_t launch_qb(const KParams &p, u64 *words, const u8 *seq, u64 len, int q,
                              int canonical, RecSpec rec, const u64 *tile_off, u8 *out,
@@ -295,14 +331,9 @@ static cudaError_t launch_qb(const KParams &p, u64 *words, const u8 *seq, u64 le
     const u64 nwin = n_windows(len, q);
     if (nwin == 0) return cudaSuccess;
     const u64 ntiles = (nwin + kQgramTile - 1) / kQgramTile;
-    if (OP == OP_CONTAINS && p.fast_random && count == nullptr) {
-        const void *fl = (const void *)qgram_lookup_kernel<C>;
-        const unsigned g = grid_for(fl, kQgramThreads, 0, ntiles);
-        qgram_lookup_kernel<C><<<g, kQgramThreads, 0, s>>>(p, words, seq, len, q, canonical,
-                                                           rec, nwin, ntiles, tile_off, out, hits);
-        count_launch();
-        return cudaGetLastError();
-    }
+    if (OP == OP_CONTAINS && p.fast_random && count == nullptr)
+        return launch_qgram_lookup<C>(p, words, seq, len, q, canonical, rec, nwin, ntiles,
+                                      tile_off, out, hits, s);
     const void *fn = (const void *)qgram_blocks_kernel<OP, C>;
     const unsigned grid = grid_for(fn, kQgramThreads, 0, ntiles);
     qgram_blocks_kernel<OP, C><<<grid, kQgramThreads, 0, s>>>(p, words, seq, len, q, canonical,
