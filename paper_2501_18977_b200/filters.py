@@ -24,6 +24,7 @@ from __future__ import annotations
 
 import ctypes
 import math
+import threading
 from dataclasses import dataclass, replace
 
 import numpy as np
@@ -217,6 +218,7 @@ class FilterConfig:
 
 
 _KIND_CODE = {"standard": 0, "blocked": 1, "blowchoc": 2}
+_HANDLE_LOCK = threading.Lock()
 
 
 class Filter:
@@ -360,12 +362,17 @@ class Filter:
 
     @property
     def handle(self):
+        """The C-ABI handle, created once (thread-safe: lookups may run from
+        several threads, as in the reference's query pool)."""
         if self._handle is None:
-            dev = self.device
-            with torch.cuda.device(dev):
-                h = ctypes.c_void_p()
-                check(lib().bc_filter_create(ctypes.byref(self._kernel_args()), ctypes.byref(h)))
-            self._handle = h.value
+            with _HANDLE_LOCK:
+                if self._handle is None:
+                    dev = self.device
+                    with torch.cuda.device(dev):
+                        h = ctypes.c_void_p()
+                        check(lib().bc_filter_create(ctypes.byref(self._kernel_args()),
+                                                     ctypes.byref(h)))
+                    self._handle = h.value
         return self._handle
 
     # -- batched operations (the hot path) --------------------------------------------------

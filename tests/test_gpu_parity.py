@@ -631,3 +631,24 @@ def test_qgram_read_matrix_records(canonical):
         del pk
     with pytest.raises(ValueError):
         bb.encode_qgrams(enc, reads, record_len=150)
+
+
+def test_concurrent_lookups_from_threads(golden):
+    """The reference's query pool (cli.py:133-140) calls contains_many from
+    several threads on one filter: same answers as one call."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    meta, _ = golden
+    case = meta["cfg1"]
+    f = bb.Filter.from_config(config_of(case))
+    keys, probes = probes_of(case)
+    f.insert_many(keys)
+    parts = np.array_split(probes, 8)
+    with ThreadPoolExecutor(8) as pool:
+        got = np.concatenate(list(pool.map(f.contains_many, parts)))
+    assert sha(got.astype(np.uint8)) == case["out_sha256"]
+    g = bb.Filter.from_config(config_of(case))  # handle created under contention
+    g.storage.load_words(f.storage.words)
+    with ThreadPoolExecutor(8) as pool:
+        counts = list(pool.map(g.count_hits, parts))
+    assert sum(counts) == case["hits_pos"] + case["hits_neg"]
