@@ -323,7 +323,37 @@ def config_cases() -> None:
         json.dump(cases, fh, separators=(",", ":"))
 
 
+def spec_cases() -> None:
+    """Hash parameters the reference derives (Filter._derive_hashes,
+    filters.py:252-263) for seeded configurations: shard, block and bit
+    multipliers and ranges (spec_cases.json)."""
+    import random
+
+    rng = random.Random(11)
+    cases = []
+    for _ in range(300):
+        kind = rng.choice(["standard", "blocked", "blowchoc", "blowchoc"])
+        kw = dict(kind=kind, k=rng.randrange(1, 24), seed=rng.randrange(0, 2**64),
+                  n_capacity=rng.randrange(1, 10**6))
+        if kind == "blowchoc":
+            kw["choices"] = rng.randrange(2, 9)
+        if kind != "standard":
+            kw["shards"] = rng.choice([1, 1, 2, 3, 8])
+            kw["strategy"] = rng.choice(["random", "distinct"])
+            kw["block_bits"] = rng.choice([512, 512, 64, 256, 1024])
+        f = Filter.from_config(FilterConfig(**kw))
+        cases.append({
+            "config": kw,
+            "shard": [f.shard_spec.a, f.shard_spec.b],
+            "blocks": [[h.a, h.b] for h in f.block_specs],
+            "bits": [[h.a, h.b] for h in f.bit_specs],
+        })
+    with open(os.path.join(OUT, "spec_cases.json"), "w") as fh:
+        json.dump(cases, fh, separators=(",", ":"))
+
+
 def main() -> None:
+    spec_cases()
     config_cases()
     bwch_files()
     store: dict = {}

@@ -231,3 +231,21 @@ def test_config_validation_matches_reference_fixture():
         except Exception as exc:  # noqa: BLE001
             got = {"ok": False, "error": type(exc).__name__, "message": str(exc)}
         assert got == want, case["config"]
+
+
+def test_hash_derivation_matches_reference_fixture():
+    """Shard, block and bit multipliers/ranges derived from the seed equal the
+    reference's for 300 seeded configurations (tests/golden/spec_cases.json,
+    written by make_golden.py from the reference)."""
+    import json
+    import os
+
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "spec_cases.json")
+    with open(path) as fh:
+        cases = json.load(fh)
+    assert len(cases) == 300
+    for case in cases:
+        f = bb.Filter.from_config(bb.FilterConfig(**case["config"]))
+        assert [f.shard_spec.a, f.shard_spec.b] == case["shard"], case["config"]
+        assert [[h.a, h.b] for h in f.block_specs] == case["blocks"], case["config"]
+        assert [[h.a, h.b] for h in f.bit_specs] == case["bits"], case["config"]
