@@ -520,7 +520,8 @@ def run_ours(args, cfg):
                  "synthetic: reference key streams even_keys(n, 11) / odd_keys(., 12) "
                  "generated on the device (bit-identical to numpy), seeded 50/50 mix"),
         "config": {"workload": cfg["workload"], "insert_mode": mode,
-                   "parallelism": (f"build from per-rank key slices + OR all-reduce "
+                   "parallelism": ("single GPU" if world == 1 else
+                                   f"build from per-rank key slices + OR all-reduce "
                                    f"(all-to-all, OR fold, all-gather), lookups dp{world}"
                                    if split else
                                    f"build on rank 0 + NCCL broadcast, lookups dp{world}"),
