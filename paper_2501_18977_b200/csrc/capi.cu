@@ -266,24 +266,25 @@ static int ensure_ordered_scratch(bc_filter *f, cudaStream_t s) {
     if (const char *e = std::getenv("BC_ORDERED_CHUNK")) chunk = std::strtoull(e, nullptr, 10);
     chunk = std::max<u64>(chunk, 256);
     chunk = std::min<u64>(chunk, 1ull << 24);
-    // Claim slots: one per block up to 2^24 blocks, else 2^24 slots with the
-    // blocks hashed onto them (spurious conflicts only delay commits).
-    // Measured (bench.py --insert-mode ordered): cfg5 (M = 2^27) 1966 ->
-    // 2095 Mkeys/s with 2^24 hashed slots, and 2 GB -> 256 MB of claim tags;
-    // cfg3 (M = 2^23) loses with fewer slots than blocks (1550 at 2^22, 1098
-    // at 2^20 vs 1761).  BC_ORDERED_SLOTS overrides (0 = one per block).
+    // Claim slots: one per block up to 2^23 blocks, else 2^23 slots with the
+    // blocks hashed onto them (spurious conflicts only delay commits).  Two
+    // arrays of 2^23 u32 claims are 64 MiB, inside the persisting L2
+    // set-aside (79 MiB on B200) the ordered launch puts them under.
+    // Measured (bench.py --insert-mode ordered, tiled commits): cfg5
+    // (M = 2^27) 4518 Mkeys/s with 2^23 slots vs 2810 with 2^24 (128 MiB, no
+    // window).  BC_ORDERED_SLOTS overrides (0 = one per block).
     u64 slots = M;
-    u64 want = 1ull << 24;
+    u64 want = 1ull << 23;
     if (const char *e = std::getenv("BC_ORDERED_SLOTS")) want = std::strtoull(e, nullptr, 10);
     if (want) {
         u64 pow2 = 1;
         while (pow2 < want) pow2 <<= 1;
         if (pow2 < M) slots = pow2;
     }
-    // two claim arrays: the sliding-window kernel claims for round r + 1
-    // while round r's claims are being checked (the fixed-chunk kernel,
-    // BC_ORDERED_WINDOW=0, uses one array of M)
-    const u64 owner_words = std::max<u64>(2 * slots, M);
+    // two arrays of u32 claims: the sliding-window kernel claims for round
+    // r + 1 while round r's claims are being checked (the fixed-chunk kernel,
+    // BC_ORDERED_WINDOW=0, uses one array of M u64 round-tagged claims)
+    const u64 owner_words = ordered_owner_words(M, slots);
     CUDA_TRY(cudaMalloc(&f->d_owner, sizeof(u64) * owner_words));
     CUDA_TRY(cudaMalloc(&f->d_lists, sizeof(u32) * 2 * chunk));
     CUDA_TRY(cudaMalloc(&f->d_state, sizeof(u32) * 4));

@@ -404,24 +404,69 @@ __global__ void __launch_bounds__(256) ordered_kernel(const __grid_constant__ KP
 //    run near-empty at the tail of a chunk.
 // Keys enter in index order, so every earlier key that shares a block with a
 // pending key is either committed or pending (and then wins that block):
-// the result is the sequential one.  Claims carry (~round) in the high word,
-// so stale values of older rounds (and launches) always lose.  state[0] is
-// the round counter; state[1..3] are rotating append counters (round r
-// appends to counter r % 3 and zeroes counter (r + 1) % 3, last read two
-// syncs ago).
+// the result is the sequential one.
+//
+// Claims are the 32-bit key index itself (launches cover < 2^32 - 1 keys;
+// 0xffffffff is "unclaimed").  Every claimed slot has exactly one winner,
+// which checks it in the next round and then resets it to unclaimed -- after
+// reading all of its slots, so a key whose candidates share a slot still
+// sees its own claim.  Losers read the slot before or after that reset and
+// see a tag that is not theirs either way.  The last round of a launch has no
+// losers (nothing is claimed in it), so both arrays are all-unclaimed between
+// launches and no round number is needed in the tags: the arrays are half
+// the size of 64-bit round-tagged claims, which lets the claims of a 2^23-block
+// filter (64 MiB) stay L2-resident under a persisting window.  state[0] is
+// the round counter (array parity); state[1..3] are rotating append counters
+// (round r appends to counter r % 3 and zeroes counter (r + 1) % 3, last
+// read two syncs ago).
 // Claim slot of block b: the block itself (slot_shift == 0), or a
 // multiplicative hash into 2^(64 - slot_shift) slots.  Two blocks sharing a
 // slot only make their keys wait for each other (a spurious conflict); keys
 // that share a block always share its slot, so commits stay exact, and the
-// oldest pending key still wins every slot it claims.  Hashed slots keep the
-// claim arrays L2-sized for filters with many blocks.
+// oldest pending key still wins every slot it claims.
 __device__ __forceinline__ u64 owner_slot(u64 b, u32 slot_shift) {
     return slot_shift ? (b * 0x9E3779B97F4A7C15ull) >> slot_shift : b;
 }
 
+constexpr u32 kUnclaimed = 0xffffffffu;
+
+// Round check of pending key li: does it hold the claim on every candidate?
+// Its own claims are reset to unclaimed after all of them have been read.
+__device__ __forceinline__ bool ordered_check(const KParams &p, u32 *own_cur, u32 slot_shift,
+                                              u64 x, u32 li) {
+    u32 mine = 0;  // candidates whose slot holds this key's claim
+    for (u32 ci = 0; ci < p.c; ++ci)
+        mine |= (u32)(__ldcg(own_cur + owner_slot(block_index(p, x, ci), slot_shift)) == li)
+                << ci;
+    for (u32 ci = 0; ci < p.c; ++ci)
+        if ((mine >> ci) & 1u)
+            __stcg(own_cur + owner_slot(block_index(p, x, ci), slot_shift), kUnclaimed);
+    return mine == (1u << p.c) - 1u;
+}
+
+__device__ __forceinline__ void ordered_claim(const KParams &p, u32 *own_nxt, u32 slot_shift,
+                                              u64 x, u32 li) {
+    for (u32 ci = 0; ci < p.c; ++ci)
+        atomicMin(own_nxt + owner_slot(block_index(p, x, ci), slot_shift), li);
+}
+
+// Losers of a round go to the next pending list: one counter atomic per warp
+// (list order is irrelevant, priority is the key index).
+__device__ __forceinline__ void ordered_append(u32 *cnt, u32 *nxt, bool lose, u32 li, int lane) {
+    const u32 am = __activemask();
+    const u32 lm = __ballot_sync(am, lose);
+    if (lm) {
+        const int leader = __ffs(lm) - 1;
+        u32 base = 0;
+        if (lane == leader) base = atomicAdd(cnt, (u32)__popc(lm));
+        base = __shfl_sync(am, base, leader);
+        if (lose) nxt[base + __popc(lm & ((1u << lane) - 1u))] = li;
+    }
+}
+
 __global__ void __launch_bounds__(256) ordered_window_kernel(
     const __grid_constant__ KParams p, u64 *__restrict__ words, const u64 *__restrict__ keys,
-    u64 n, u64 window, u64 *__restrict__ owner, u64 slots, u32 slot_shift,
+    u64 n, u64 window, u32 *__restrict__ owner, u64 slots, u32 slot_shift,
     u32 *__restrict__ lists, u32 *__restrict__ state) {
     cg::grid_group grid = cg::this_grid();
     const u64 gtid = blockIdx.x * (u64)blockDim.x + threadIdx.x;
@@ -436,22 +481,18 @@ __global__ void __launch_bounds__(256) ordered_window_kernel(
     u64 mask[kMaxWpb];
     while (npend > 0 || next < n) {
         const u64 admit = min(window - npend, n - next);
-        const u64 *own_cur = owner + (round & 1u) * slots;
-        u64 *own_nxt = owner + ((round + 1u) & 1u) * slots;
-        const u64 claim_cur = (u64)(0xffffffffu - round) << 32;
-        const u64 claim_nxt = (u64)(0xffffffffu - (round + 1u)) << 32;
+        u32 *own_cur = owner + (round & 1u) * slots;
+        u32 *own_nxt = owner + ((round + 1u) & 1u) * slots;
         u32 *cnt = state + 1 + round % 3u;
         if (gtid == 0) state[1 + (round + 1u) % 3u] = 0;
         for (u64 t = gtid; t < npend + admit; t += gstride) {
             u32 li;
             bool lose = true;
+            u64 x;
             if (t < npend) {
                 li = __ldcg(cur + t);
-                const u64 x = keys[li];
-                bool win = true;
-                for (u32 ci = 0; ci < p.c; ++ci)
-                    win &= __ldcg(own_cur + owner_slot(block_index(p, x, ci), slot_shift)) ==
-                           (claim_cur | li);
+                x = keys[li];
+                const bool win = ordered_check(p, own_cur, slot_shift, x, li);
                 if (win && fast) {
                     insert_fast512(p, words, x, col);
                 } else if (win) {
@@ -461,23 +502,10 @@ __global__ void __launch_bounds__(256) ordered_window_kernel(
                 lose = !win;
             } else {
                 li = (u32)(next + (t - npend));  // newly admitted
+                x = keys[li];
             }
-            if (lose) {
-                const u64 x = keys[li];
-                for (u32 ci = 0; ci < p.c; ++ci)
-                    atomicMin((unsigned long long *)(own_nxt +
-                                                     owner_slot(block_index(p, x, ci), slot_shift)),
-                              (unsigned long long)(claim_nxt | li));
-            }
-            const u32 am = __activemask();
-            const u32 lm = __ballot_sync(am, lose);
-            if (lm) {
-                const int leader = __ffs(lm) - 1;
-                u32 base = 0;
-                if (lane == leader) base = atomicAdd(cnt, (u32)__popc(lm));
-                base = __shfl_sync(am, base, leader);
-                if (lose) nxt[base + __popc(lm & ((1u << lane) - 1u))] = li;
-            }
+            if (lose) ordered_claim(p, own_nxt, slot_shift, x, li);
+            ordered_append(cnt, nxt, lose, li, lane);
         }
         grid.sync();
         npend = __ldcg(cnt);
@@ -488,6 +516,64 @@ __global__ void __launch_bounds__(256) ordered_window_kernel(
         ++round;
     }
     if (gtid == 0) state[0] = round;
+}
+
+// The same rounds for 512-bit blocks with the random strategy (every BASELINE
+// configuration): a round's winners are committed a warp tile at a time with
+// the relaxed insert's two-phase step (masks built one lane per key, the C
+// candidates of four keys at once read with one LDG.128 per lane, the
+// reference's decision, two sector-wide REDs per key), instead of one thread
+// per key issuing 4 C loads and 8 REDs.  Winners of one round touch pairwise
+// disjoint blocks, so the blocks they read cannot change under them.
+template <int C>
+__global__ void __launch_bounds__(kTPB) ordered512_kernel(
+    const __grid_constant__ KParams p, u64 *__restrict__ words, const u64 *__restrict__ keys,
+    u64 n, u64 window, u32 *__restrict__ owner, u64 slots, u32 slot_shift,
+    u32 *__restrict__ lists, u32 *__restrict__ state) {
+    cg::grid_group grid = cg::this_grid();
+    __shared__ WarpSmem<C> smem[kWarps];
+    WarpSmem<C> &ws = smem[threadIdx.x >> 5];
+    const int lane = threadIdx.x & 31;
+    const u64 warp = blockIdx.x * (u64)kWarps + (threadIdx.x >> 5);
+    const u64 wstride = (u64)gridDim.x * kTPB;
+    u32 round = __ldcg(state);
+    u32 *cur = lists, *nxt = lists + window;
+    u64 npend = 0, next = 0;
+    while (npend > 0 || next < n) {
+        const u64 admit = min(window - npend, n - next);
+        u32 *own_cur = owner + (round & 1u) * slots;
+        u32 *own_nxt = owner + ((round + 1u) & 1u) * slots;
+        u32 *cnt = state + 1 + round % 3u;
+        if (warp == 0 && lane == 0) state[1 + (round + 1u) % 3u] = 0;
+        const u64 total = npend + admit;
+        for (u64 t0 = warp * 32; t0 < total; t0 += wstride) {  // warp-uniform
+            const u64 t = t0 + lane;
+            const bool valid = t < total;
+            u32 li = 0;
+            u64 x = 0;
+            bool win = false;
+            if (valid) {
+                li = t < npend ? __ldcg(cur + t) : (u32)(next + (t - npend));
+                x = keys[li];
+                if (t < npend) win = ordered_check(p, own_cur, slot_shift, x, li);
+            }
+            phase1<C>(p, x, win, ws, lane);
+            __syncwarp();
+            phase2<OP_INSERT, C>(p, words, ws, lane);
+            __syncwarp();
+            const bool lose = valid && !win;
+            if (lose) ordered_claim(p, own_nxt, slot_shift, x, li);
+            ordered_append(cnt, nxt, lose, li, lane);
+        }
+        grid.sync();
+        npend = __ldcg(cnt);
+        next += admit;
+        u32 *tmp = cur;
+        cur = nxt;
+        nxt = tmp;
+        ++round;
+    }
+    if (warp == 0 && lane == 0) state[0] = round;
 }
 
 template <int OP>
@@ -824,7 +910,7 @@ cudaError_t launch_blocks(int op, const KParams &p, u64 *words, const u64 *keys,
     return cudaGetLastError();
 }
 
-static bool ordered_window_enabled() {  // BC_ORDERED_WINDOW=0: fixed chunks
+bool ordered_window_mode() {  // BC_ORDERED_WINDOW=0: fixed chunks
     static const bool on = [] {
         const char *e = getenv("BC_ORDERED_WINDOW");
         return e == nullptr || atoi(e) != 0;
@@ -832,27 +918,86 @@ static bool ordered_window_enabled() {  // BC_ORDERED_WINDOW=0: fixed chunks
     return on;
 }
 
+// BC_ORDERED_TILES=0: winners committed one thread per key (insert_fast512)
+static bool ordered_tiles() {
+    static const bool on = [] {
+        const char *e = getenv("BC_ORDERED_TILES");
+        return e == nullptr || atoi(e) != 0;
+    }();
+    return on;
+}
+
+static const void *ordered512_ptr(u32 c) {
+    switch (c) {
+        case 2: return (const void *)ordered512_kernel<2>;
+        case 3: return (const void *)ordered512_kernel<3>;
+        case 4: return (const void *)ordered512_kernel<4>;
+        case 5: return (const void *)ordered512_kernel<5>;
+        case 6: return (const void *)ordered512_kernel<6>;
+        case 7: return (const void *)ordered512_kernel<7>;
+        default: return (const void *)ordered512_kernel<8>;
+    }
+}
+
+u64 ordered_owner_words(u64 num_blocks, u64 slots) {
+    // window kernel: two arrays of `slots` u32 claims; fixed-chunk kernel:
+    // one array of num_blocks u64 round-tagged claims
+    return ordered_window_mode() ? slots : num_blocks;
+}
+
 cudaError_t launch_ordered(const KParams &p, u64 *words, const u64 *keys, u64 n, u64 chunk,
                            u64 *owner, u64 slots, u32 *lists, u32 *state, cudaStream_t s) {
     if (n == 0) return cudaSuccess;
-    l2_release();
-    if (ordered_window_enabled()) {
-        // owner holds two arrays of num_blocks claims; the append counters
-        // state[1..3] start at zero, the round counter state[0] carries over
+    if (ordered_window_mode()) {
+        // the append counters state[1..3] start at zero, the round counter
+        // state[0] (array parity) carries over
         cudaError_t e = cudaMemsetAsync(state + 1, 0, 3 * sizeof(u32), s);
         if (e != cudaSuccess) return e;
-        const void *fw = (const void *)ordered_window_kernel;
+        const bool tile = p.fast_random && p.wpb == 8 && p.c >= 2 && p.c <= 8 && ordered_tiles();
+        const void *fw = tile ? ordered512_ptr(p.c) : (const void *)ordered_window_kernel;
         const unsigned grid = grid_for(fw, 256, 0, (chunk + 255) / 256);
-        KParams pp = p;
         u32 slot_shift = 0;  // identity slots when there is one per block
         if (slots < p.num_blocks) slot_shift = 64u - (u32)__builtin_ctzll(slots);
-        void *args[] = {(void *)&pp,    (void *)&words,      (void *)&keys,  (void *)&n,
-                        (void *)&chunk, (void *)&owner,      (void *)&slots, (void *)&slot_shift,
-                        (void *)&lists, (void *)&state};
-        e = cudaLaunchCooperativeKernel(fw, dim3(grid), dim3(256), args, 0, s);
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(grid);
+        cfg.blockDim = dim3(256);
+        cfg.stream = s;
+        cudaLaunchAttribute attr[2];
+        attr[0].id = cudaLaunchAttributeCooperative;
+        attr[0].val.cooperative = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        // the claim arrays (not the filter: ordered builds run on filters of
+        // any size) persist in L2 when they fit: every pending key reads and
+        // claims c random slots per round
+        size_t bytes = 0;
+        float hit = 0.f;
+        const size_t claim_bytes = sizeof(u32) * 2 * slots;
+        if (l2_window(claim_bytes, &bytes, &hit)) {
+            attr[1].id = cudaLaunchAttributeAccessPolicyWindow;
+            attr[1].val.accessPolicyWindow.base_ptr = owner;
+            attr[1].val.accessPolicyWindow.num_bytes = bytes;
+            attr[1].val.accessPolicyWindow.hitRatio = hit;
+            attr[1].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+            attr[1].val.accessPolicyWindow.missProp = cudaAccessPropertyNormal;
+            cfg.numAttrs = 2;
+        }
         count_launch();
-        return e;
+        u32 *own = reinterpret_cast<u32 *>(owner);
+        if (!tile)
+            return cudaLaunchKernelEx(&cfg, ordered_window_kernel, p, words, keys, n, chunk, own,
+                                      slots, slot_shift, lists, state);
+        switch (p.c) {
+#define BC_ORD_C(c)                                                                          \
+    case c:                                                                                  \
+        return cudaLaunchKernelEx(&cfg, ordered512_kernel<c>, p, words, keys, n, chunk, own, \
+                                  slots, slot_shift, lists, state);
+            BC_ORD_C(2) BC_ORD_C(3) BC_ORD_C(4) BC_ORD_C(5) BC_ORD_C(6) BC_ORD_C(7) BC_ORD_C(8)
+#undef BC_ORD_C
+        }
+        return cudaErrorInvalidValue;
     }
+    l2_release();
     const void *fn = (const void *)ordered_kernel;
     const unsigned grid = grid_for(fn, 256, 0, (chunk + 255) / 256);
     KParams pp = p;

@@ -28,8 +28,11 @@ cudaError_t launch_blocks(int op, const KParams &p, u64 *words, const u64 *keys,
                           u8 *out, unsigned long long *hits, cudaStream_t s);
 
 // Exact stream-order insert for c >= 2 (claim rounds, one cooperative launch).
-// owner: two arrays of `slots` claim tags (slots == num_blocks: one per block,
-// else a power of two, blocks hashed onto slots).
+// owner: the claim arrays, ordered_owner_words(num_blocks, slots) u64 words,
+// all-ones before the first launch (slots == num_blocks: one per block, else
+// a power of two, blocks hashed onto slots).  n < 2^32 - 1 per launch.
+bool ordered_window_mode();
+u64 ordered_owner_words(u64 num_blocks, u64 slots);
 cudaError_t launch_ordered(const KParams &p, u64 *words, const u64 *keys, u64 n, u64 chunk,
                            u64 *owner, u64 slots, u32 *lists, u32 *state, cudaStream_t s);
 

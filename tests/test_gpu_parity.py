@@ -533,10 +533,13 @@ def test_ordered_build_with_hashed_claim_slots(golden, slots):
 
 @pytest.mark.parametrize("name,env", [("cfg2_small", {"BC_LOOKUP_PIPE": "0"}),
                                       ("bc3_k12_20k", {"BC_ORDERED_WINDOW": "0"}),
-                                      ("cfg1", {"BC_ORDERED_WINDOW": "0"})])
+                                      ("cfg1", {"BC_ORDERED_WINDOW": "0"}),
+                                      ("bc3_k12_20k", {"BC_ORDERED_TILES": "0"}),
+                                      ("cfg1", {"BC_ORDERED_TILES": "0"})])
 def test_fallback_kernels_match_reference(golden, name, env):
     """The non-default kernel variants kept behind switches (unpipelined
-    single-choice lookups, fixed-chunk exact inserts) still give the
+    single-choice lookups, fixed-chunk exact inserts, exact inserts that
+    commit one thread per key) still give the
     reference's bits and answers."""
     meta, _ = golden
     case = meta[name]
