@@ -525,8 +525,11 @@ __global__ void __launch_bounds__(256) ordered_window_kernel(
 // reference's decision, two sector-wide REDs per key), instead of one thread
 // per key issuing 4 C loads and 8 REDs.  Winners of one round touch pairwise
 // disjoint blocks, so the blocks they read cannot change under them.
+#ifndef BC_ORD_MINB
+#define BC_ORD_MINB 3  // <= 80 registers: 3 CTAs per SM (cfg3 +4%, cfg5 +8% over 1 CTA)
+#endif
 template <int C>
-__global__ void __launch_bounds__(kTPB) ordered512_kernel(
+__global__ void __launch_bounds__(kTPB, BC_ORD_MINB) ordered512_kernel(
     const __grid_constant__ KParams p, u64 *__restrict__ words, const u64 *__restrict__ keys,
     u64 n, u64 window, u32 *__restrict__ owner, u64 slots, u32 slot_shift,
     u32 *__restrict__ lists, u32 *__restrict__ state) {
@@ -546,24 +549,45 @@ __global__ void __launch_bounds__(kTPB) ordered512_kernel(
         u32 *cnt = state + 1 + round % 3u;
         if (warp == 0 && lane == 0) state[1 + (round + 1u) % 3u] = 0;
         const u64 total = npend + admit;
-        for (u64 t0 = warp * 32; t0 < total; t0 += wstride) {  // warp-uniform
+        // warp-uniform tiles; the next tile's list entry and key are loaded
+        // while the current tile's candidate blocks are read and committed
+        u64 t0 = warp * 32;
+        u32 li = 0;
+        u64 x = 0;
+        if (t0 + lane < total) {
+            const u64 t = t0 + lane;
+            li = t < npend ? __ldcg(cur + t) : (u32)(next + (t - npend));
+            x = keys[li];
+        }
+        while (t0 < total) {
             const u64 t = t0 + lane;
             const bool valid = t < total;
-            u32 li = 0;
-            u64 x = 0;
-            bool win = false;
-            if (valid) {
-                li = t < npend ? __ldcg(cur + t) : (u32)(next + (t - npend));
-                x = keys[li];
-                if (t < npend) win = ordered_check(p, own_cur, slot_shift, x, li);
+            const bool win = valid && t < npend && ordered_check(p, own_cur, slot_shift, x, li);
+            const bool lose = valid && !win;
+            if (lose) ordered_claim(p, own_nxt, slot_shift, x, li);
+            // reserve the losers' list slots now, store them after the commit
+            const u32 lm = __ballot_sync(kFull, lose);
+            u32 base = 0;
+            if (lm && lane == 0) base = atomicAdd(cnt, (u32)__popc(lm));
+            const u64 t1 = t0 + wstride;
+            u32 li_n = 0;
+            u64 x_n = 0;
+            if (t1 + lane < total) {
+                const u64 tn = t1 + lane;
+                li_n = tn < npend ? __ldcg(cur + tn) : (u32)(next + (tn - npend));
+                x_n = keys[li_n];
             }
             phase1<C>(p, x, win, ws, lane);
             __syncwarp();
             phase2<OP_INSERT, C>(p, words, ws, lane);
             __syncwarp();
-            const bool lose = valid && !win;
-            if (lose) ordered_claim(p, own_nxt, slot_shift, x, li);
-            ordered_append(cnt, nxt, lose, li, lane);
+            if (lm) {
+                base = __shfl_sync(kFull, base, 0);
+                if (lose) nxt[base + __popc(lm & ((1u << lane) - 1u))] = li;
+            }
+            li = li_n;
+            x = x_n;
+            t0 = t1;
         }
         grid.sync();
         npend = __ldcg(cnt);
