@@ -577,10 +577,12 @@ __global__ void __launch_bounds__(kTPB, BC_ORD_MINB) ordered512_kernel(
                 li_n = tn < npend ? __ldcg(cur + tn) : (u32)(next + (tn - npend));
                 x_n = keys[li_n];
             }
-            phase1<C>(p, x, win, ws, lane);
-            __syncwarp();
-            phase2<OP_INSERT, C>(p, words, ws, lane);
-            __syncwarp();
+            if (__ballot_sync(kFull, win)) {  // tiles of admitted keys only claim
+                phase1<C>(p, x, win, ws, lane);
+                __syncwarp();
+                phase2<OP_INSERT, C>(p, words, ws, lane);
+                __syncwarp();
+            }
             if (lm) {
                 base = __shfl_sync(kFull, base, 0);
                 if (lose) nxt[base + __popc(lm & ((1u << lane) - 1u))] = li;
