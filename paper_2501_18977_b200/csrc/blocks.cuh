@@ -219,11 +219,11 @@ __device__ __forceinline__ void read_masks(const WarpSmem<C> &ws, int lane, bool
 // ---- phase 2: four lanes per key -------------------------------------------------
 // Lookups: returns the answers of the group's four keys packed one per byte
 // (key 4g + p in byte p), identical in the four lanes of the group.
-template <int OP, int C>
+template <int OP, int C, int UNRX = 0>
 __device__ __forceinline__ u32 phase2(const KParams &p, u64 *words, WarpSmem<C> &ws,
                                       int lane) {
     constexpr bool kNoLoad = (OP == OP_INSERT && C == 1);
-    constexpr int UNR = kNoLoad ? 4 : relaxed_unroll(C);
+    constexpr int UNR = kNoLoad ? 4 : (UNRX ? UNRX : relaxed_unroll(C));
     constexpr int CL = kNoLoad ? 1 : C;
     const int g = lane >> 2, s = lane & 3;
     const uint4 *w4 = reinterpret_cast<const uint4 *>(words);

@@ -525,6 +525,9 @@ __global__ void __launch_bounds__(256) ordered_window_kernel(
 // reference's decision, two sector-wide REDs per key), instead of one thread
 // per key issuing 4 C loads and 8 REDs.  Winners of one round touch pairwise
 // disjoint blocks, so the blocks they read cannot change under them.
+#ifndef BC_ORD_UNR
+#define BC_ORD_UNR 0  // keys per load step of the commit (0: relaxed_unroll(C))
+#endif
 #ifndef BC_ORD_MINB
 #define BC_ORD_MINB 3  // <= 80 registers: 3 CTAs per SM (cfg3 +4%, cfg5 +8% over 1 CTA)
 #endif
@@ -580,7 +583,7 @@ __global__ void __launch_bounds__(kTPB, BC_ORD_MINB) ordered512_kernel(
             if (__ballot_sync(kFull, win)) {  // tiles of admitted keys only claim
                 phase1<C>(p, x, win, ws, lane);
                 __syncwarp();
-                phase2<OP_INSERT, C>(p, words, ws, lane);
+                phase2<OP_INSERT, C, BC_ORD_UNR>(p, words, ws, lane);
                 __syncwarp();
             }
             if (lm) {
