@@ -773,7 +773,11 @@ static int host_pipeline(bc_filter *f, u64 *words, const u64 *h_keys, u64 n, int
     for (u64 off = 0; off < n && rc == BC_OK; off += chunk, ++chunk_i) {
         const int b = (int)(chunk_i & 1);
         const u64 len = std::min(chunk, n - off);
-        CUDA_TRY(cudaEventSynchronize(st->done[b]));  // buffer b is free again
+        // The device buffers of slot b are reused in stream order (copy stream
+        // b queues behind its previous D2H, which waited for that chunk's
+        // kernel); only the host staging buffers need the host to wait.
+        if (!keys_pinned || (h_out && !out_pinned))
+            CUDA_TRY(cudaEventSynchronize(st->done[b]));  // staging slot b is free again
         if (pend[b].live && h_out && !out_pinned)
             std::memcpy(h_out + pend[b].off, st->h_out[b], pend[b].len);
         pend[b].live = false;
