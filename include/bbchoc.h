@@ -187,6 +187,30 @@ BC_API int bc_format_answers(const uint64_t *h_keys, const uint8_t *h_answers, u
 BC_API int bc_parse_keys_text(const char *h_text, uint64_t len, uint64_t *h_keys, uint64_t cap,
                               uint64_t *consumed, uint64_t *lines, uint64_t *n_keys);
 
+/* ---- multi-GPU replica merge over peer memory (distributed.py) ----------------
+ * CUDA IPC mapping of a device buffer for the other ranks: the 64-byte handle
+ * of the allocation holding d_ptr and d_ptr's offset in it (torch's caching
+ * allocator hands out interior pointers).  bc_ipc_import maps a peer's
+ * allocation on the current device (lazy peer access) and returns the
+ * buffer's address there; bc_ipc_close unmaps it. */
+BC_API int bc_ipc_export(const void *d_ptr, void *handle, uint64_t *offset);
+BC_API int bc_ipc_import(const void *handle, uint64_t offset, void **d_ptr);
+BC_API int bc_ipc_close(void *d_ptr, uint64_t offset);
+
+/* Words per rank range of the merge: ceil(nwords / world) rounded up to 32. */
+BC_API int bc_peer_span(uint64_t nwords, int world, uint64_t *span);
+
+/* Bitwise-OR all-reduce of `world` replicas of nwords words, this rank's
+ * share: ORs word range `rank` of every replica (h_peer_words: host array of
+ * the replicas' addresses on this device, own one included) and stores the
+ * result into that range of every replica -- one kernel, loads and stores
+ * over NVLink.  Ranges of different ranks are disjoint and no kernel waits on
+ * another; the caller runs every rank's call between two cross-rank barriers
+ * (all replicas written before, all calls finished after).  Replaces the
+ * NCCL all-to-all + OR + all-gather of the order-free multi-GPU build. */
+BC_API int bc_or_allreduce_peers(uint64_t *const *h_peer_words, int world, int rank,
+                                 uint64_t nwords, void *stream);
+
 /* Thread-local description of the last error on this thread. */
 BC_API const char *bc_last_error(void);
 

@@ -35,6 +35,14 @@ static int fail(int code, const char *fmt, ...) {
     return code;
 }
 
+namespace bc {
+// error entry for the other translation units (peer.cu)
+int set_error(int code, const char *msg) {
+    g_err = msg;
+    return code;
+}
+}  // namespace bc
+
 #define CUDA_TRY(expr)                                                                   \
     do {                                                                                 \
         cudaError_t e__ = (expr);                                                        \

@@ -34,6 +34,9 @@ with gloo and the oracle standing in for the kernels.
 
 from __future__ import annotations
 
+import ctypes
+import os
+
 import numpy as np
 import torch
 import torch.distributed as dist
@@ -150,15 +153,124 @@ def gather_subfilters(filt, group=None) -> None:
     filt.storage.device_modified()
 
 
+# -- replica merge over peer memory ------------------------------------------------------
+
+def _peer_mode() -> int:
+    """BC_PEER_ALLREDUCE: 0 never, 1 always (any backend, e.g. gloo ranks
+    sharing a GPU in tests), unset: NCCL groups whose GPUs reach each other."""
+    v = os.environ.get("BC_PEER_ALLREDUCE")
+    return -1 if v is None else int(v)
+
+
+_PEER_CACHE: dict = {}  # (group, ptr, numel) -> PeerReplicas or None
+_IPC_OPEN: dict = {}    # exported allocation handle -> its base address here
+
+
+class PeerReplicas:
+    """The ranks' replicas of one word tensor, mapped into this process
+    (CUDA IPC; lazy peer access over NVLink)."""
+
+    def __init__(self, words: torch.Tensor, group=None):
+        from . import _native
+
+        L = _native.lib()
+        rank, world = _rank_world(group)
+        handle = (ctypes.c_ubyte * 64)()
+        off = ctypes.c_uint64()
+        _native.check(L.bc_ipc_export(ctypes.c_void_p(words.data_ptr()), handle,
+                                      ctypes.byref(off)))
+        infos = [None] * world
+        dist.all_gather_object(infos, (bytes(handle), off.value), group=group)
+        self.world, self.rank, self.nwords = world, rank, words.numel()
+        self.ptrs = (ctypes.c_uint64 * world)()
+        for j, (h, o) in enumerate(infos):
+            if j == rank:
+                self.ptrs[j] = words.data_ptr()
+                continue
+            if h not in _IPC_OPEN:
+                base = ctypes.c_void_p()
+                _native.check(L.bc_ipc_import(h, 0, ctypes.byref(base)))
+                _IPC_OPEN[h] = base.value
+            self.ptrs[j] = _IPC_OPEN[h] + o
+        self.words = words  # keeps the local replica (and its mapping) alive
+
+    def or_allreduce(self, stream) -> None:
+        from . import _native
+
+        _native.check(_native.lib().bc_or_allreduce_peers(
+            self.ptrs, self.world, self.rank, self.nwords, ctypes.c_void_p(stream)))
+
+
+def _peer_replicas(words: torch.Tensor, group):
+    """Cached PeerReplicas when every rank can map every other rank's
+    replica, else None.  The decision is collective (all ranks agree)."""
+    mode = _peer_mode()
+    if mode == 0 or not words.is_cuda or not words.is_contiguous():
+        return None
+    if mode != 1 and dist.get_backend(group) != "nccl":
+        return None
+    key = (id(group), words.data_ptr(), words.numel())
+    if key in _PEER_CACHE:
+        return _PEER_CACHE[key]
+    rank, world = _rank_world(group)
+    dev = words.device.index
+    devs = [None] * world
+    dist.all_gather_object(devs, dev, group=group)
+    ok = words.data_ptr() % 16 == 0 and world <= 16 and all(
+        d == dev or torch.cuda.can_device_access_peer(dev, d) for d in devs)
+    oks = [None] * world
+    dist.all_gather_object(oks, bool(ok), group=group)
+    reps = None
+    if all(oks):
+        try:
+            reps = PeerReplicas(words, group)
+            good = True
+        except (RuntimeError, ValueError, MemoryError):
+            good = False
+        flags = [None] * world
+        dist.all_gather_object(flags, good, group=group)
+        if not all(flags):
+            reps = None
+    _PEER_CACHE[key] = reps
+    return reps
+
+
+def _device_barrier(group, device) -> None:
+    """Every rank's earlier work on its current stream is finished before
+    anything after this runs on any rank: a one-element NCCL all-reduce on
+    the stream, or (other backends) a host sync plus a barrier."""
+    if dist.get_backend(group) == "nccl":
+        dist.all_reduce(torch.zeros(1, device=device), group=group)
+    else:
+        torch.cuda.synchronize(device)
+        dist.barrier(group=group)
+
+
+def or_allreduce_peer_(words: torch.Tensor, reps: PeerReplicas, group=None) -> torch.Tensor:
+    """OR all-reduce through peer memory: each rank's single kernel ORs its
+    word range over all replicas and writes it back into all of them
+    (bc_or_allreduce_peers), between two cross-rank barriers."""
+    _device_barrier(group, words.device)
+    reps.or_allreduce(torch.cuda.current_stream(words.device).cuda_stream)
+    _device_barrier(group, words.device)
+    return words
+
+
 def or_allreduce_(words: torch.Tensor, group=None) -> torch.Tensor:
-    """In-place bitwise-OR all-reduce of an int64 word tensor (NCCL has no OR
-    reduction): an all-to-all of W equal word ranges (the reduce-scatter
+    """In-place bitwise-OR all-reduce of an int64 word tensor.
+
+    GPUs that reach each other's memory (NVLink / NVSwitch) use one peer-memory
+    kernel per rank (or_allreduce_peer_).  Otherwise, since NCCL has no OR
+    reduction: an all-to-all of W equal word ranges (the reduce-scatter
     layout), an OR fold of the W pieces each rank received, and an all-gather
-    of the folded ranges.  Every rank moves 2 (W-1)/W of the array, like a
-    ring all-reduce.  Stream-ordered, no host synchronisation."""
+    of the folded ranges.  Every rank moves 2 (W-1)/W of the array either way,
+    like a ring all-reduce.  Stream-ordered, no host synchronisation."""
     rank, world = _rank_world(group)
     if world == 1:
         return words
+    reps = _peer_replicas(words, group)
+    if reps is not None:
+        return or_allreduce_peer_(words, reps, group)
     n = words.numel()
     span = -(-n // world)
     pad = span * world - n

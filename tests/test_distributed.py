@@ -188,3 +188,80 @@ def test_nccl_collectives_on_device():
     if 4 % world:  # the test filter has 4 shards
         world = 1
     mp.spawn(_nccl_worker, args=(world, free_port()), nprocs=world, join=True)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world,nwords", [(2, 1 << 16), (3, 1 << 16), (4, 12_345), (5, 999),
+                                          (8, (1 << 20) + 7), (1, 33)])
+def test_peer_or_kernel_emulated_ranks(world, nwords):
+    """bc_or_allreduce_peers over W replicas held on one GPU (the ranks
+    emulated in one process, each rank's call launched in turn): every
+    replica ends up as the OR of all of them, odd tails included."""
+    import ctypes
+
+    import torch
+
+    from paper_2501_18977_b200 import _native
+
+    L = _native.lib()
+    g = torch.Generator(device="cuda").manual_seed(world * 1000 + nwords)
+    reps = [torch.randint(-2**63, 2**63 - 1, (nwords,), dtype=torch.int64, device="cuda",
+                          generator=g) for _ in range(world)]
+    want = reps[0].clone()
+    for r in reps[1:]:
+        want |= r
+    ptrs = (ctypes.c_uint64 * world)(*[r.data_ptr() for r in reps])
+    stream = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    for rank in range(world):
+        _native.check(L.bc_or_allreduce_peers(ptrs, world, rank, nwords, stream))
+    torch.cuda.synchronize()
+    for r in reps:
+        assert torch.equal(r, want)
+    span = ctypes.c_uint64()
+    _native.check(L.bc_peer_span(nwords, world, ctypes.byref(span)))
+    assert span.value % 32 == 0 and span.value * world >= nwords
+    with pytest.raises(ValueError):
+        _native.check(L.bc_or_allreduce_peers(ptrs, world, world, nwords, stream))
+
+
+def _peer_worker(rank, world, port):
+    import torch
+
+    import paper_2501_18977_b200 as bb
+    from paper_2501_18977_b200 import distributed as D
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    os.environ["BC_PEER_ALLREDUCE"] = "1"
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        for kind, k, n in (("blocked", 9, 30_001), ("standard", 5, 12_345)):
+            cfg = bb.FilterConfig(kind=kind, k=k, n_capacity=n, seed=23)
+            keys = bb.even_keys(n, 3)
+            # an allocation ahead of the words, so they sit at an offset inside
+            # the caching allocator's segment
+            pad = torch.empty(1000 + 77 * rank, dtype=torch.uint8, device="cuda")
+            f = bb.Filter.from_config(cfg)
+            D.build_subfilters(f, torch.from_numpy(keys).cuda())
+            assert D._peer_replicas(D._words_i64(f), None) is not None
+            ref = orc.make_filter(kind=kind, k=k, n_capacity=n, seed=23)
+            ref.insert_many(keys)
+            assert np.array_equal(f.storage.words, ref.words)
+            assert f.inserted == n
+            # a second merge reuses the mappings and changes nothing
+            D.or_allreduce_(D._words_i64(f))
+            f.storage.device_modified()
+            assert np.array_equal(f.storage.words, ref.words)
+            del pad
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_peer_or_allreduce_two_processes_one_gpu():
+    """The peer-memory merge end to end: two ranks (gloo barriers) sharing
+    cuda:0 exchange CUDA IPC handles of their replicas, each runs its one
+    merge kernel, and both hold the sequential build.  No kernel waits on the
+    other rank (the barriers are on the host)."""
+    mp.spawn(_peer_worker, args=(2, free_port()), nprocs=2, join=True)
