@@ -194,6 +194,50 @@ def test_cfg3_properties_full_size():
     assert hist.total_set_bits == f.storage.total_set_bits()
 
 
+@pytest.mark.parametrize("name,c,k,size_bits,n", [
+    # config 3 geometry: 512 MiB, M = 2^23 (one claim slot per block)
+    ("cfg3", 3, 16, 16 * 2**28, 2**23),
+    # config 5 geometry: 8 GiB, M = 2^27 blocks hashed onto 2^23 claim slots
+    ("cfg5", 2, 11, 2**36, 2**22),
+])
+def test_exact_order_full_geometry_matches_oracle(name, c, k, size_bits, n):
+    """Exact-order builds on the full-size filters of configs 3 and 5 (only
+    the key count is reduced so the sequential oracle finishes in seconds):
+    bit-identical words, and identical answers on a mixed probe set."""
+    cfg = bb.FilterConfig(kind="blowchoc", k=k, choices=c, size_bits=size_bits, seed=1)
+    keys = bb.even_keys(n, 11)
+    f = bb.Filter.from_config(cfg, insert_mode="ordered")
+    f.insert_many(torch.from_numpy(keys).cuda())
+    o = orc.make_filter("blowchoc", k=k, choices=c, size_bits=size_bits, seed=1)
+    o.insert_many(keys)
+    got = f.storage.d_words.cpu().numpy()
+    assert np.array_equal(got, o.words), f"{name}: exact-order words differ from the oracle"
+    probes = np.concatenate([keys[::5], bb.odd_keys(2**20, 12)])
+    ans = f.contains_many(torch.from_numpy(probes).cuda()).cpu().numpy()
+    np.testing.assert_array_equal(ans, o.contains_many(probes, threads=8))
+
+
+def test_exact_order_full_size_split_and_reinsert():
+    """Config 3 at full size (2^28 keys, exact order): building in two calls
+    gives the same bits as one call (stream order is the only input), and
+    inserting the stream again changes nothing (every key is then a no-op
+    under the reference's rule, _kernels.py:156-160)."""
+    n = 2**28
+    cfg = bb.FilterConfig(kind="blowchoc", k=16, choices=3, size_bits=16 * n, seed=1)
+    keys = bb.even_keys(n, 11, device="cuda")
+    f = bb.Filter.from_config(cfg, insert_mode="ordered")
+    f.insert_many(keys)
+    one = f.storage.d_words.clone()
+    g = bb.Filter.from_config(cfg, insert_mode="ordered")
+    h = 3 * n // 7
+    g.insert_many(keys[:h])
+    g.insert_many(keys[h:])
+    assert torch.equal(g.storage.d_words, one)
+    f.insert_many(keys)
+    assert torch.equal(f.storage.d_words, one)
+    assert f.count_hits(keys[::101]) == keys[::101].numel()
+
+
 # -- edge cases ------------------------------------------------------------------------
 
 @pytest.mark.parametrize("kind,c", [("standard", None), ("blocked", 1), ("blowchoc", 2),
