@@ -238,6 +238,36 @@ def test_exact_order_full_size_split_and_reinsert():
     assert f.count_hits(keys[::101]) == keys[::101].numel()
 
 
+def test_relaxed_vs_exact_order_cfg5_full_size():
+    """Config 5 at full size (8 GiB, k = 11, 1.2 x 2^32 keys): the relaxed
+    build against the bit-exact build of the same stream, with the relaxed
+    tolerances of SURVEY §8(a) written here: no false negatives, FPR within
+    0.1 in log2 plus 3 sigma, mean block load within 1 bit, load variance
+    within 15%, histogram total variation <= 0.05."""
+    import math
+
+    from paper_2501_18977_b200.analysis import histogram_distance
+
+    n = int(1.2 * 2**32)
+    cfg = bb.FilterConfig(kind="blowchoc", k=11, choices=2, size_bits=2**36, seed=1)
+    keys = bb.even_keys(n, 11, device="cuda")
+    neg = bb.odd_keys(2**26, 12, device="cuda")
+    res = {}
+    for mode in ("ordered", "relaxed"):
+        f = bb.Filter.from_config(cfg, insert_mode=mode)
+        f.insert_many(keys)
+        assert f.count_hits(keys[::997]) == keys[::997].numel(), f"{mode}: false negatives"
+        res[mode] = (f.count_hits(neg), bb.block_load_histogram(f))
+        del f
+        torch.cuda.empty_cache()
+    (fp_e, h_e), (fp_r, h_r) = res["ordered"], res["relaxed"]
+    sigma = math.sqrt(1 / fp_e + 1 / fp_r) / math.log(2)  # stderr of the log2 ratio
+    assert abs(math.log2(fp_r / fp_e)) <= 0.1 + 3 * sigma, (fp_e, fp_r)
+    assert abs(h_r.mean_load - h_e.mean_load) <= 1.0
+    assert abs(h_r.variance / h_e.variance - 1) <= 0.15
+    assert histogram_distance(h_r.counts, h_e.counts) <= 0.05
+
+
 # -- edge cases ------------------------------------------------------------------------
 
 @pytest.mark.parametrize("kind,c", [("standard", None), ("blocked", 1), ("blowchoc", 2),
