@@ -382,6 +382,37 @@ def test_eval_hash_many_and_routing(golden):
     np.testing.assert_array_equal(f.route_many(keys), [f.shard_of(int(v)) for v in keys])
 
 
+def test_eval_hash_modulus_paths():
+    """The device remainder (single-multiply Barrett) for odd
+    and even ranges from 3 to 2^64 - 1, against Python's exact integers --
+    random keys plus keys that put a*x just below, on and above multiples
+    of b."""
+    rng = np.random.default_rng(8)
+    ranges = [3, 5, 6, 1000, 1_572_864, 32_812_500, (1 << 30) - 2, (1 << 30) - 1,
+              (1 << 30) + 1, (1 << 30) + 2, 3 << 40, (1 << 63) + 7, (1 << 64) - 1]
+    ranges += [int(v) for v in rng.integers(3, 1 << 30, 20)]
+    for b in ranges:
+        if b & (b - 1) == 0:
+            continue
+        for a in (0x9E3779B97F4A7C15, int(rng.integers(1, 2**63)) * 2 + 1):
+            a |= 1 << 63 | 1
+            x = [int(v) for v in rng.integers(0, 2**64, 2000, dtype=np.uint64)]
+            ainv = pow(a, -1, 1 << 64)
+            for t in (1, 2, 3, 7):  # a*x = t*b + {-1, 0, 1} (mod 2^64)
+                for d in (-1, 0, 1):
+                    x.append(((t * b + d) % (1 << 64)) * ainv % (1 << 64))
+            x += [0, 1, (1 << 64) - 1, 1 << 63]
+            keys = np.array(x, dtype=np.uint64)
+            got = bb.eval_hash_many(bb.HashSpec(a=a, b=b), keys)
+            want = []
+            for v in x:
+                ax = a * v % (1 << 64)
+                if b % 2 == 0:
+                    ax ^= ax >> 32
+                want.append(ax % b)
+            np.testing.assert_array_equal(got, np.array(want, dtype=np.uint64), err_msg=str(b))
+
+
 def test_sharded_build_equals_sequential():
     cfg = bb.FilterConfig(kind="blowchoc", k=7, n_capacity=20_000, choices=3, shards=8, seed=4)
     keys = bb.even_keys(20_000, 5)
