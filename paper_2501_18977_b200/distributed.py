@@ -170,28 +170,9 @@ class PeerReplicas:
     """The ranks' replicas of one word tensor, mapped into this process
     (CUDA IPC; lazy peer access over NVLink)."""
 
-    def __init__(self, words: torch.Tensor, group=None):
-        from . import _native
-
-        L = _native.lib()
-        rank, world = _rank_world(group)
-        handle = (ctypes.c_ubyte * 64)()
-        off = ctypes.c_uint64()
-        _native.check(L.bc_ipc_export(ctypes.c_void_p(words.data_ptr()), handle,
-                                      ctypes.byref(off)))
-        infos = [None] * world
-        dist.all_gather_object(infos, (bytes(handle), off.value), group=group)
-        self.world, self.rank, self.nwords = world, rank, words.numel()
-        self.ptrs = (ctypes.c_uint64 * world)()
-        for j, (h, o) in enumerate(infos):
-            if j == rank:
-                self.ptrs[j] = words.data_ptr()
-                continue
-            if h not in _IPC_OPEN:
-                base = ctypes.c_void_p()
-                _native.check(L.bc_ipc_import(h, 0, ctypes.byref(base)))
-                _IPC_OPEN[h] = base.value
-            self.ptrs[j] = _IPC_OPEN[h] + o
+    def __init__(self, words: torch.Tensor, rank: int, ptrs: list):
+        self.world, self.rank, self.nwords = len(ptrs), rank, words.numel()
+        self.ptrs = (ctypes.c_uint64 * len(ptrs))(*ptrs)
         self.words = words  # keeps the local replica (and its mapping) alive
 
     def or_allreduce(self, stream) -> None:
@@ -201,9 +182,44 @@ class PeerReplicas:
             self.ptrs, self.world, self.rank, self.nwords, ctypes.c_void_p(stream)))
 
 
+def _export(words: torch.Tensor):
+    """(IPC handle bytes, offset) of this rank's replica, or None."""
+    from . import _native
+
+    try:
+        handle = (ctypes.c_ubyte * 64)()
+        off = ctypes.c_uint64()
+        _native.check(_native.lib().bc_ipc_export(ctypes.c_void_p(words.data_ptr()), handle,
+                                                  ctypes.byref(off)))
+        return bytes(handle), off.value
+    except (RuntimeError, ValueError, MemoryError):
+        return None
+
+
+def _import(infos: list, rank: int, words: torch.Tensor):
+    """This process's addresses of every rank's replica, or None."""
+    from . import _native
+
+    ptrs = []
+    try:
+        for j, (h, o) in enumerate(infos):
+            if j == rank:
+                ptrs.append(words.data_ptr())
+                continue
+            if h not in _IPC_OPEN:
+                base = ctypes.c_void_p()
+                _native.check(_native.lib().bc_ipc_import(h, 0, ctypes.byref(base)))
+                _IPC_OPEN[h] = base.value
+            ptrs.append(_IPC_OPEN[h] + o)
+    except (RuntimeError, ValueError, MemoryError):
+        return None
+    return ptrs
+
+
 def _peer_replicas(words: torch.Tensor, group):
     """Cached PeerReplicas when every rank can map every other rank's
-    replica, else None.  The decision is collective (all ranks agree)."""
+    replica, else None.  Every rank runs the same collectives in the same
+    order whatever fails locally, and the decision is the AND over ranks."""
     mode = _peer_mode()
     if mode == 0 or not words.is_cuda or not words.is_contiguous():
         return None
@@ -213,24 +229,23 @@ def _peer_replicas(words: torch.Tensor, group):
     if key in _PEER_CACHE:
         return _PEER_CACHE[key]
     rank, world = _rank_world(group)
+
+    def agree(local):
+        out = [None] * world
+        dist.all_gather_object(out, local, group=group)
+        return out
+
     dev = words.device.index
-    devs = [None] * world
-    dist.all_gather_object(devs, dev, group=group)
+    devs = agree(dev)
     ok = words.data_ptr() % 16 == 0 and world <= 16 and all(
         d == dev or torch.cuda.can_device_access_peer(dev, d) for d in devs)
-    oks = [None] * world
-    dist.all_gather_object(oks, bool(ok), group=group)
     reps = None
-    if all(oks):
-        try:
-            reps = PeerReplicas(words, group)
-            good = True
-        except (RuntimeError, ValueError, MemoryError):
-            good = False
-        flags = [None] * world
-        dist.all_gather_object(flags, good, group=group)
-        if not all(flags):
-            reps = None
+    if all(agree(bool(ok))):
+        infos = agree(_export(words))
+        if all(i is not None for i in infos):
+            ptrs = _import(infos, rank, words)
+            if all(agree(ptrs is not None)):
+                reps = PeerReplicas(words, rank, ptrs)
     _PEER_CACHE[key] = reps
     return reps
 
