@@ -16,6 +16,9 @@ restatement of the reference's own implementation timed beside it:
            bases/s
   tsv      CLI query output (cli.py:141-142 f-string per key) -- native
            bc_format_answers vs the f-string join
+  standard the standard (flat) Bloom kind (_kernels.py:214-237) at config 2's
+           size -- not a BASELINE config; k random bits per key anywhere in
+           the array (parity: tests/test_gpu_parity.py golden 'standard')
 
 usage: python tools/bench_next.py [--out profiles/r1/bench_next.jsonl]
 The oracle is not used: the CPU restatements here are numpy / Python
@@ -217,6 +220,26 @@ def row_tsv(bb, torch, out):
          "parity": "identical" if ok else "DIFF"})
 
 
+def row_standard(bb, torch, out):
+    n = 1 << 26
+    f = bb.Filter.from_config(bb.FilterConfig(kind="standard", k=12, size_bits=12 * n, seed=1))
+    keys = bb.even_keys(n, 11, device=f.device)
+    q = torch.cat([keys[: n], bb.odd_keys(n, 12, device=f.device)])
+    res = torch.empty(q.numel(), dtype=torch.uint8, device=f.device)
+
+    def build():
+        f.storage.d_words.zero_()
+        f.insert_many(keys)
+
+    ins = cuda_ms(build)
+    look = cuda_ms(lambda: f.contains_many(q, out=res))
+    fn = int((res[:n] == 0).sum().item())
+    out({"row": "standard", "workload": "standard Bloom, k = 12, 12 b/key (96 MiB), 2^26 keys, "
+         "2^27 lookups (50% positive)", "insert_mkeys_s": round(n / ins / 1e3, 1),
+         "lookup_mkeys_s": round(2 * n / look / 1e3, 1), "false_negatives": fn,
+         "fpr": float(res[n:].float().mean().item())})
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--out", default=None)
@@ -238,6 +261,7 @@ def main():
         row_keys(bb, torch, out, tmp)
         row_fasta(bb, torch, out, tmp)
         row_tsv(bb, torch, out)
+        row_standard(bb, torch, out)
     if args.out:
         with open(args.out, "w") as fh:
             fh.writelines(json.dumps(d) + "\n" for d in lines)
