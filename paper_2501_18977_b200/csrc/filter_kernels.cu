@@ -8,9 +8,12 @@
 //                            tile's hashing overlapped with the loads
 //   lookup512_kernel<C, K>   lookups: staged blocks, early exit over choices
 //   lookup512_pipe_kernel<K> single-choice lookups, two tiles in flight
-//   ordered_window_kernel    exact stream-order insert for c >= 2: claim
-//                            rounds over a sliding window, one cooperative
-//                            launch (ordered_kernel: fixed-chunk variant)
+//   ordered512_kernel<C>     exact stream-order insert for c >= 2, 512-bit
+//                            blocks: claim rounds over a sliding window, one
+//                            cooperative launch, winners committed a warp
+//                            tile at a time
+//   ordered_window_kernel    the same rounds for any geometry, thread-per-key
+//                            commits (ordered_kernel: fixed-chunk variant)
 //   flat_kernel<OP>          standard Bloom filter (k global bits)
 //   hist512_kernel / hist_generic_kernel   per-block popcount tally
 //   eval_hash_kernel         one hash over a key array (routing)
