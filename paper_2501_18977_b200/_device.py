@@ -9,6 +9,8 @@ from __future__ import annotations
 
 import ctypes
 
+import warnings
+
 import numpy as np
 import torch
 
@@ -90,8 +92,15 @@ def as_device_bytes(seq, device: torch.device) -> torch.Tensor:
         return seq.to(device=device, dtype=torch.uint8).contiguous()
     if isinstance(seq, np.ndarray):
         raw = np.ascontiguousarray(seq, dtype=np.uint8).reshape(-1)
-        return torch.from_numpy(raw).to(device) if raw.size else \
-            torch.empty(0, dtype=torch.uint8, device=device)
+        if not raw.size:
+            return torch.empty(0, dtype=torch.uint8, device=device)
+        if raw.flags.writeable:
+            return torch.from_numpy(raw).to(device)
+        # a read-only array (np.frombuffer over bytes) is only copied from, so
+        # torch's warning about non-writable tensors does not apply
+        with warnings.catch_warnings():
+            warnings.simplefilter("ignore", UserWarning)
+            return torch.from_numpy(raw).to(device)
     if isinstance(seq, str):
         seq = seq.encode("ascii", errors="replace")
     raw = np.frombuffer(bytes(seq), dtype=np.uint8)

@@ -102,3 +102,56 @@ def test_fuzz_against_oracle(seed):
         np.testing.assert_array_equal(f.contains_many(probes), want, err_msg=f"{mode} {d}")
         got = f.contains_many(torch.from_numpy(probes).cuda()).cpu().numpy()
         np.testing.assert_array_equal(got, want, err_msg=f"{mode} (device keys) {d}")
+
+
+def draw_sequence(rng, n: int) -> bytes:
+    """Mostly ACGT, some lower case, N runs and other bytes."""
+    alphabet = np.frombuffer(b"ACGTacgtNnX>\n", dtype=np.uint8)
+    p = np.array([22, 22, 22, 22, 2, 2, 2, 2, 1.5, 0.5, 0.5, 0.2, 0.3])
+    return alphabet[rng.choice(len(alphabet), size=n, p=p / p.sum())].tobytes()
+
+
+@pytest.mark.parametrize("seed", range(max(10, N_CASES // 3)))
+def test_fuzz_qgrams_against_oracle(seed):
+    """Fused q-gram encode / insert / lookup on random sequences (N runs,
+    lower case, separators, q = 1..32, canonical or not, fixed-length
+    records or one joined sequence) against the oracle's encode_qgrams
+    composed with its insert and lookups."""
+    rng = np.random.default_rng(5000 + seed)
+    q = int(rng.integers(1, 33))
+    canonical = bool(rng.random() < 0.7)
+    enc = bb.QGramEncoder(q=q, canonical=canonical)
+    record_len = int(rng.integers(q, 400)) if rng.random() < 0.4 else None
+    n = int(rng.integers(0, 150_000))
+    if record_len:
+        n -= n % record_len
+    seq = draw_sequence(rng, n)
+    if record_len:
+        recs = [seq[i:i + record_len] for i in range(0, n, record_len)]
+        keys = np.concatenate([orc.encode_qgrams(r, q, canonical) for r in recs]) if recs \
+            else np.empty(0, dtype=np.uint64)
+    else:
+        keys = orc.encode_qgrams(seq, q, canonical)
+    got = bb.encode_qgrams(enc, np.frombuffer(seq, dtype=np.uint8), record_len=record_len) \
+        if record_len else bb.encode_qgrams(enc, seq)
+    np.testing.assert_array_equal(got, keys)
+    kind, c = (("blocked", 1), ("blowchoc", 2), ("blowchoc", 3))[seed % 3]
+    k = int(rng.integers(1, 17))
+    cfg = bb.FilterConfig(kind=kind, k=k, choices=c, size_bits=max(512, 12 * len(keys)),
+                          seed=seed)
+    f = bb.Filter.from_config(cfg)  # exact order
+    o = orc.make_filter(kind, k=k, choices=c, size_bits=max(512, 12 * len(keys)), seed=seed)
+    data = np.frombuffer(seq, dtype=np.uint8)
+    assert f.insert_qgrams(enc, data, record_len=record_len) == len(keys)
+    o.insert_many(keys)
+    np.testing.assert_array_equal(f.storage.words, o.words)
+    probe = draw_sequence(rng, int(rng.integers(0, 50_000)) // (record_len or 1) *
+                          (record_len or 1))
+    pk = (np.concatenate([orc.encode_qgrams(probe[i:i + record_len], q, canonical)
+                          for i in range(0, len(probe), record_len)] or
+                         [np.empty(0, dtype=np.uint64)])
+          if record_len else orc.encode_qgrams(probe, q, canonical))
+    pdata = np.frombuffer(probe, dtype=np.uint8)
+    ans = f.contains_qgrams(enc, pdata, record_len=record_len)
+    np.testing.assert_array_equal(np.asarray(ans).astype(bool), o.contains_many(pk).astype(bool))
+    assert f.count_qgram_hits(enc, pdata, record_len=record_len) == int(o.contains_many(pk).sum())
