@@ -95,9 +95,21 @@ def row_hist(bb, torch, out):
         ms = cuda_ms(lambda: f.storage.histogram())
         got = f.storage.histogram()
         nbytes = d.numel() * 8
-        line = {"row": "hist", "workload": label, "gpu_ms": round(ms, 4),
-                "gbs": round(nbytes / ms / 1e6, 1), "peak_gbs": peak, "peak_source": src,
-                "frac": round(nbytes / ms / 1e6 / peak, 4)}
+        # the kernel alone (bc_block_histogram into a resident counts buffer),
+        # without the counts' zeroing, D2H copy and host sync of the API call
+        import ctypes
+
+        from paper_2501_18977_b200 import _native
+
+        counts = torch.zeros(513, dtype=torch.int64, device=d.device)
+        stream = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+        kms = cuda_ms(lambda: _native.check(_native.lib().bc_block_histogram(
+            ctypes.c_void_p(d.data_ptr()), f.storage.num_blocks, 512,
+            ctypes.c_void_p(counts.data_ptr()), stream)), reps=20)
+        line = {"row": "hist", "workload": label, "call_ms": round(ms, 4),
+                "kernel_ms": round(kms, 4), "kernel_gbs": round(nbytes / kms / 1e6, 1),
+                "peak_gbs": peak, "peak_source": src,
+                "kernel_frac": round(nbytes / kms / 1e6 / peak, 4)}
         if mib <= 512:
             host = d.cpu().numpy().view(np.uint64)
             t = wall(lambda: ref_hist(host, 8))
