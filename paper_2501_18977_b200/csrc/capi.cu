@@ -3,7 +3,9 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
+#include <condition_variable>
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
@@ -11,6 +13,7 @@
 #include <map>
 #include <mutex>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/bbchoc.h"
@@ -689,6 +692,94 @@ extern "C" int bc_parse_keys_text(const char *h_text, uint64_t len, uint64_t *h_
     return BC_OK;
 }
 
+// ---- parallel host copies -------------------------------------------------------------
+// Pageable caller buffers are staged through pinned memory with memcpy; one
+// thread copies ~14 GB/s, a quarter of the PCIe Gen5 link, so the copies of a
+// chunk are split over a small persistent pool (BC_COPY_THREADS, default
+// min(8, cores / 2); 1 disables).
+namespace {
+class CopyPool {
+   public:
+    static CopyPool &get() {
+        static CopyPool pool;
+        return pool;
+    }
+
+    void copy(void *dst, const void *src, size_t n) {
+        const size_t kMin = 1 << 20;  // below this one thread is faster
+        const int parts = (int)std::min<size_t>(workers_.size() + 1, std::max<size_t>(1, n / kMin));
+        if (parts <= 1) {
+            std::memcpy(dst, src, n);
+            return;
+        }
+        const size_t per = (n / parts + 63) & ~size_t(63);
+        {
+            std::lock_guard<std::mutex> lk(mu_);
+            for (int i = 1; i < parts; ++i) {
+                const size_t a = std::min(n, per * i), b = std::min(n, per * (i + 1));
+                if (b > a) {
+                    jobs_.push_back({static_cast<char *>(dst) + a,
+                                     static_cast<const char *>(src) + a, b - a});
+                    ++pending_;
+                }
+            }
+        }
+        cv_.notify_all();
+        std::memcpy(dst, src, std::min(n, per));  // the caller's share
+        std::unique_lock<std::mutex> lk(mu_);
+        done_.wait(lk, [&] { return pending_ == 0; });
+    }
+
+   private:
+    struct Job {
+        char *dst;
+        const char *src;
+        size_t n;
+    };
+
+    CopyPool() {
+        int t = 0;
+        if (const char *e = std::getenv("BC_COPY_THREADS")) t = std::atoi(e) - 1;
+        else t = (int)std::min(8u, std::max(1u, std::thread::hardware_concurrency() / 2)) - 1;
+        for (int i = 0; i < t; ++i) workers_.emplace_back([this] { run(); });
+    }
+
+    ~CopyPool() {
+        {
+            std::lock_guard<std::mutex> lk(mu_);
+            stop_ = true;
+        }
+        cv_.notify_all();
+        for (auto &w : workers_) w.join();
+    }
+
+    void run() {
+        for (;;) {
+            Job j;
+            {
+                std::unique_lock<std::mutex> lk(mu_);
+                cv_.wait(lk, [&] { return stop_ || !jobs_.empty(); });
+                if (stop_ && jobs_.empty()) return;
+                j = jobs_.back();
+                jobs_.pop_back();
+            }
+            std::memcpy(j.dst, j.src, j.n);
+            std::lock_guard<std::mutex> lk(mu_);
+            if (--pending_ == 0) done_.notify_all();
+        }
+    }
+
+    std::vector<std::thread> workers_;
+    std::vector<Job> jobs_;
+    std::mutex mu_;
+    std::condition_variable cv_, done_;
+    int pending_ = 0;
+    bool stop_ = false;
+};
+
+void host_copy(void *dst, const void *src, size_t n) { CopyPool::get().copy(dst, src, n); }
+}  // namespace
+
 // ---- host-buffer entry points ---------------------------------------------------------
 // Per-device staging: two pinned key buffers, two pinned answer buffers, two
 // device key/answer buffers and two copy streams, so the copy of chunk i+1
@@ -787,11 +878,11 @@ static int host_pipeline(bc_filter *f, u64 *words, const u64 *h_keys, u64 n, int
         if (!keys_pinned || (h_out && !out_pinned))
             CUDA_TRY(cudaEventSynchronize(st->done[b]));  // staging slot b is free again
         if (pend[b].live && h_out && !out_pinned)
-            std::memcpy(h_out + pend[b].off, st->h_out[b], pend[b].len);
+            host_copy(h_out + pend[b].off, st->h_out[b], pend[b].len);
         pend[b].live = false;
         const u64 *src = h_keys + off;
         if (!keys_pinned) {
-            std::memcpy(st->h_keys[b], src, sizeof(u64) * len);
+            host_copy(st->h_keys[b], src, sizeof(u64) * len);
             src = st->h_keys[b];
         }
         CUDA_TRY(cudaMemcpyAsync(st->d_keys[b], src, sizeof(u64) * len, cudaMemcpyHostToDevice,
@@ -816,7 +907,7 @@ static int host_pipeline(bc_filter *f, u64 *words, const u64 *h_keys, u64 n, int
     for (int b = 0; b < 2; ++b) {
         CUDA_TRY(cudaEventSynchronize(st->done[b]));
         if (pend[b].live && h_out && !out_pinned)
-            std::memcpy(h_out + pend[b].off, st->h_out[b], pend[b].len);
+            host_copy(h_out + pend[b].off, st->h_out[b], pend[b].len);
     }
     if (d_hits) {
         unsigned long long v = 0;
