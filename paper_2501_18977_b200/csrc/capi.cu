@@ -16,6 +16,8 @@
 #include <thread>
 #include <vector>
 
+#include <unistd.h>
+
 #include "../../include/bbchoc.h"
 #include "launch.h"
 
@@ -708,7 +710,7 @@ class CopyPool {
     void copy(void *dst, const void *src, size_t n) {
         const size_t kMin = 1 << 20;  // below this one thread is faster
         const int parts = (int)std::min<size_t>(workers_.size() + 1, std::max<size_t>(1, n / kMin));
-        if (parts <= 1) {
+        if (parts <= 1 || getpid() != pid_) {  // a forked child has no workers
             std::memcpy(dst, src, n);
             return;
         }
@@ -737,7 +739,7 @@ class CopyPool {
         size_t n;
     };
 
-    CopyPool() {
+    CopyPool() : pid_(getpid()) {
         int t = 0;
         if (const char *e = std::getenv("BC_COPY_THREADS")) t = std::atoi(e) - 1;
         else t = (int)std::min(8u, std::max(1u, std::thread::hardware_concurrency() / 2)) - 1;
@@ -775,6 +777,7 @@ class CopyPool {
     std::condition_variable cv_, done_;
     int pending_ = 0;
     bool stop_ = false;
+    const pid_t pid_;
 };
 
 void host_copy(void *dst, const void *src, size_t n) { CopyPool::get().copy(dst, src, n); }
