@@ -714,7 +714,7 @@ class CopyPool {
             std::memcpy(dst, src, n);
             return;
         }
-        const size_t per = (n / parts + 63) & ~size_t(63);
+        const size_t per = ((n + parts - 1) / parts + 63) & ~size_t(63);  // parts * per >= n
         {
             std::lock_guard<std::mutex> lk(mu_);
             for (int i = 1; i < parts; ++i) {

@@ -775,6 +775,26 @@ def test_qgram_read_matrix_records(canonical):
         bb.encode_qgrams(enc, reads, record_len=150)
 
 
+@pytest.mark.parametrize("n", [1, 7, 4097, 131_075, 393_219, 1_048_579, 3_145_733,
+                               (1 << 22) + 11, 3 * (1 << 22) + 5])
+def test_host_buffers_awkward_lengths(n):
+    """Pageable numpy keys and answers of awkward lengths (staged through
+    pinned chunks by the parallel host copy) give the device path's bits and
+    answers."""
+    cfg = bb.FilterConfig(kind="blowchoc", k=9, choices=2, size_bits=10 * max(n, 1000), seed=3)
+    keys = bb.even_keys(n, 5)
+    probes = np.concatenate([keys[::2], bb.odd_keys(n, 6)])
+    f = bb.Filter.from_config(cfg)
+    g = bb.Filter.from_config(cfg)
+    f.insert_many(keys)                                   # host path
+    g.insert_many(torch.from_numpy(keys).cuda())          # device path
+    assert torch.equal(f.storage.d_words, g.storage.d_words)
+    want = g.contains_many(torch.from_numpy(probes).cuda()).cpu().numpy()
+    np.testing.assert_array_equal(f.contains_many(probes), want)
+    np.testing.assert_array_equal(f.contains_many(probes[1:]), want[1:])  # unaligned start
+    assert f.count_hits(probes) == int(want.sum())
+
+
 def test_concurrent_lookups_from_threads(golden):
     """The reference's query pool (cli.py:133-140) calls contains_many from
     several threads on one filter: same answers as one call."""
