@@ -532,7 +532,7 @@ __global__ void __launch_bounds__(256) ordered_window_kernel(
 #define BC_ORD_UNR 0  // keys per load step of the commit (0: relaxed_unroll(C))
 #endif
 #ifndef BC_ORD_MINB
-#define BC_ORD_MINB 3  // <= 80 registers: 3 CTAs per SM (cfg3 +4%, cfg5 +8% over 1 CTA)
+#define BC_ORD_MINB 3  // <= 80 registers: 3 CTAs per SM (cfg3 +4%, cfg5 +8% over 2 CTAs at 102)
 #endif
 template <int C>
 __global__ void __launch_bounds__(kTPB, BC_ORD_MINB) ordered512_kernel(
