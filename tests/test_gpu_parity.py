@@ -113,10 +113,11 @@ def test_relaxed_build_tolerance(golden, name):
         exact.insert_many(keys)
         assert sha(exact.storage.words) == case["words_sha256"]
         a, b = hist.counts, bb.block_load_histogram(exact).counts
-        if f.num_blocks < 1 << 15:
-            # below 2^15 blocks the per-load-value sampling noise alone is near
-            # 0.05 (cfg5_small: 8192 blocks, ~0.05 measured), so compare the
-            # shapes on loads binned by 4
+        if f.num_blocks < 1 << 16:
+            # below 2^16 blocks the per-load-value sampling noise alone comes
+            # near 0.05 (max of 10 relaxed builds, tools/relaxed_spread_probe.py:
+            # 0.054 at 8192 blocks, 0.042 at 32768), so compare the shapes on
+            # loads binned by 4
             w = 4
             a = np.add.reduceat(a, np.arange(0, len(a), w))
             b = np.add.reduceat(b, np.arange(0, len(b), w))
