@@ -15,7 +15,8 @@ Streams hold up to 40,000 keys (10% of the seeds: up to 600,000), so filters
 range from one block to tens of thousands, relaxed inserts run in M/2-key
 slices or one capped launch, and exact-order inserts use one or many rounds.
 
-FUZZ_CASES=<n> widens the sweep (default 60 seeds).
+FUZZ_CASES=<n> widens the sweep (default 60 seeds); FUZZ_OFFSET=<m> moves it
+to another slice of the seed space.
 """
 
 import os
@@ -30,6 +31,7 @@ from oracle import oracle as orc
 pytestmark = pytest.mark.gpu
 
 N_CASES = int(os.environ.get("FUZZ_CASES", "60"))
+OFFSET = int(os.environ.get("FUZZ_OFFSET", "0"))  # another slice of the seed space
 COSTS = {"exp": (0, (1.2, 2.0, 8.0)), "mix": (1, (0.0, 0.5, 3.0)), "la": (2, (0.0, 1.0, 4.0))}
 
 
@@ -78,7 +80,7 @@ def build_pair(d, mode):
 
 @pytest.mark.parametrize("seed", range(N_CASES))
 def test_fuzz_against_oracle(seed):
-    d = draw(1000 + seed)
+    d = draw(1000 + OFFSET + seed)
     keys = bb.even_keys(d["n"], d["key_seed"])
     probes = np.concatenate([keys[::3], bb.odd_keys(4099, d["key_seed"] + 1)])
     bounds = [0] + d["cuts"] + [d["n"]]
@@ -117,7 +119,7 @@ def test_fuzz_qgrams_against_oracle(seed):
     lower case, separators, q = 1..32, canonical or not, fixed-length
     records or one joined sequence) against the oracle's encode_qgrams
     composed with its insert and lookups."""
-    rng = np.random.default_rng(5000 + seed)
+    rng = np.random.default_rng(5000 + OFFSET + seed)
     q = int(rng.integers(1, 33))
     canonical = bool(rng.random() < 0.7)
     enc = bb.QGramEncoder(q=q, canonical=canonical)
