@@ -347,7 +347,13 @@ static int insert_device(bc_filter *f, u64 *words, const u64 *keys, u64 n, int m
         // keep at most M/2 keys in flight (FPR within ~3%): one
         // persistent launch whose grid holds <= M/2 keys (256 per CTA) at a time,
         // or, for filters under 512 blocks, launches of M/2 keys each
-        const u64 per = std::max<u64>(1, f->kp.num_blocks / 2);
+        // BC_RELAXED_INFLIGHT_PCT (experiments only): keys in flight as a
+        // percentage of M instead of the 50% the tolerance is stated for
+        static const u64 pct = [] {
+            const char *e = std::getenv("BC_RELAXED_INFLIGHT_PCT");
+            return e ? std::max<u64>(1, std::strtoull(e, nullptr, 10)) : 50ull;
+        }();
+        const u64 per = std::max<u64>(1, f->kp.num_blocks * pct / 100);
         if (per >= 256) {
             KParams kp = f->kp;
             kp.max_ctas = (u32)std::min<u64>(per / 256, 0xffffffffu);
