@@ -806,6 +806,31 @@ def test_host_buffers_awkward_lengths(n):
     assert f.count_hits(probes) == int(want.sum())
 
 
+def test_concurrent_host_inserts_into_separate_filters():
+    """Several threads insert pageable numpy streams into their own filters at
+    once (shared per-device staging and copy pool): each filter equals its
+    sequentially built twin."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    cfgs = [bb.FilterConfig(kind=kind, k=k, choices=c, size_bits=12 * (1 << 21), seed=s)
+            for s, (kind, k, c) in enumerate([("blocked", 12, 1), ("blowchoc", 14, 2),
+                                              ("blowchoc", 16, 3), ("standard", 9, None)])]
+    streams = [bb.even_keys((1 << 21) + 17 * i, 40 + i) for i in range(len(cfgs))]
+
+    def build(i):
+        f = bb.Filter.from_config(cfgs[i])
+        f.insert_many(streams[i][: len(streams[i]) // 3])
+        f.insert_many(streams[i][len(streams[i]) // 3:])
+        return f.storage.d_words.clone()
+
+    with ThreadPoolExecutor(len(cfgs)) as pool:
+        got = list(pool.map(build, range(len(cfgs))))
+    for i, cfg in enumerate(cfgs):
+        g = bb.Filter.from_config(cfg)
+        g.insert_many(torch.from_numpy(streams[i]).cuda())
+        assert torch.equal(got[i], g.storage.d_words), cfg
+
+
 def test_concurrent_lookups_from_threads(golden):
     """The reference's query pool (cli.py:133-140) calls contains_many from
     several threads on one filter: same answers as one call."""
