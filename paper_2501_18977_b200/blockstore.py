@@ -75,16 +75,31 @@ class BlockArray:
         self._host_valid = False
 
     # -- host mirror ---------------------------------------------------------------
-    @property
-    def words(self) -> np.ndarray:
+    def _synced_host(self) -> np.ndarray:
+        """The host mirror, current; lending is the caller's business."""
         if self._host is None:
             self._host = np.zeros(self.num_words, dtype=np.uint64)
             self._host_valid = self._d_words is None
         if not self._host_valid:
             self._host[:] = self._d_words.cpu().numpy()
             self._host_valid = True
-        self._host_lent = True
         return self._host
+
+    @property
+    def words(self) -> np.ndarray:
+        """The host mirror, writable like the reference's numpy attribute
+        (its tests write through it, test_filters.py:103): it is lent out, and
+        the next device operation uploads it."""
+        host = self._synced_host()
+        self._host_lent = True
+        return host
+
+    def words_readonly(self) -> np.ndarray:
+        """A read-only view of the current host mirror; reading does not
+        force the next device operation to re-upload the filter."""
+        v = self._synced_host().view()
+        v.flags.writeable = False
+        return v
 
     def load_words(self, words: np.ndarray) -> None:
         words = np.asarray(words, dtype=np.uint64)
@@ -118,23 +133,27 @@ class BlockArray:
         lo = block * self.words_per_block
         return self.words[lo:lo + self.words_per_block]
 
+    def _block_readonly(self, block: int) -> np.ndarray:
+        lo = block * self.words_per_block
+        return self.words_readonly()[lo:lo + self.words_per_block]
+
     def set_bits(self, block: int, addrs) -> None:
         m = self._mask_of(self._addresses(block, addrs))
         np.bitwise_or(self.block_words(block), m, out=self.block_words(block))
 
     def test_all(self, block: int, addrs) -> bool:
         m = self._mask_of(self._addresses(block, addrs))
-        return not np.any(m & ~self.block_words(block))
+        return not np.any(m & ~self._block_readonly(block))
 
     def popcount_block(self, block: int) -> int:
         self._addresses(block, ())
-        return int(np.bitwise_count(self.block_words(block)).sum())
+        return int(np.bitwise_count(self._block_readonly(block)).sum())
 
     def simulate_insertion(self, block: int, addrs) -> tuple:
         """(j, a): set bits after inserting ``addrs`` and how many of them are
         new; the block is left untouched (a == 0: all already set)."""
         m = self._mask_of(self._addresses(block, addrs))
-        view = self.block_words(block)
+        view = self._block_readonly(block)
         new = int(np.bitwise_count(m & ~view).sum())
         return int(np.bitwise_count(view).sum()) + new, new
 
@@ -146,6 +165,6 @@ class BlockArray:
 
     def total_set_bits(self) -> int:
         if self._host_valid or self._d_words is None:
-            return int(popcount_words(self.words).sum())
+            return int(popcount_words(self.words_readonly()).sum())
         counts = self.histogram()
         return int((np.arange(counts.shape[0], dtype=np.int64) * counts).sum())

@@ -98,7 +98,11 @@ struct bc_filter {
     std::mutex mu;  // ordered-insert scratch
     u64 *d_owner = nullptr;
     u32 *d_lists = nullptr;
+    u64 *d_lkeys = nullptr;
     u32 *d_state = nullptr;
+    // completion of the last ordered launch: the scratch is per handle, so a
+    // launch on another stream waits for it (one writer at a time)
+    cudaEvent_t ord_done = nullptr;
     u64 chunk = 0;
     u64 slots = 0;        // claim slots per owner array
     u64 owner_words = 0;  // allocated u64 claim tags
@@ -249,7 +253,9 @@ extern "C" void bc_filter_destroy(bc_filter *f) {
     cudaFree(f->d_rank);
     cudaFree(f->d_owner);
     cudaFree(f->d_lists);
+    cudaFree(f->d_lkeys);
     cudaFree(f->d_state);
+    if (f->ord_done) cudaEventDestroy(f->ord_done);
     bc::l2_release();
     cudaSetDevice(prev);
     delete f;
@@ -264,8 +270,11 @@ static int check_device(bc_filter *f) {
     return BC_OK;
 }
 
-// Ordered-insert scratch: owner[M] (u64), two pending lists of `chunk` u32,
-// state = {round, counter0, counter1}.
+// Ordered-insert scratch: the claim arrays, two pending lists of `chunk`
+// entries (u32 stream index + u64 key), state = {round, counter0..2}.  All
+// of it is allocated into locals and published only once every allocation
+// and initialisation succeeded, so a failed attempt leaves the handle
+// without scratch (the next insert retries) instead of half-initialised.
 static int ensure_ordered_scratch(bc_filter *f, cudaStream_t s) {
     if (f->d_owner) return BC_OK;
     const u64 M = f->kp.num_blocks;
@@ -298,15 +307,58 @@ static int ensure_ordered_scratch(bc_filter *f, cudaStream_t s) {
     // r + 1 while round r's claims are being checked (the fixed-chunk kernel,
     // BC_ORDERED_WINDOW=0, uses one array of M u64 round-tagged claims)
     const u64 owner_words = ordered_owner_words(M, slots);
-    CUDA_TRY(cudaMalloc(&f->d_owner, sizeof(u64) * owner_words));
-    CUDA_TRY(cudaMalloc(&f->d_lists, sizeof(u32) * 2 * chunk));
-    CUDA_TRY(cudaMalloc(&f->d_state, sizeof(u32) * 4));
-    CUDA_TRY(cudaMemsetAsync(f->d_owner, 0xff, sizeof(u64) * owner_words, s));
-    CUDA_TRY(cudaMemsetAsync(f->d_state, 0, sizeof(u32) * 4, s));
+    u64 *owner = nullptr, *lkeys = nullptr;
+    u32 *lists = nullptr, *state = nullptr;
+    cudaEvent_t done = nullptr;
+    cudaError_t e = cudaMalloc(&owner, sizeof(u64) * owner_words);
+    if (e == cudaSuccess) e = cudaMalloc(&lists, sizeof(u32) * 2 * chunk);
+    if (e == cudaSuccess) e = cudaMalloc(&lkeys, sizeof(u64) * 2 * chunk);
+    if (e == cudaSuccess) e = cudaMalloc(&state, sizeof(u32) * 4);
+    if (e == cudaSuccess) e = cudaMemsetAsync(owner, 0xff, sizeof(u64) * owner_words, s);
+    if (e == cudaSuccess) e = cudaMemsetAsync(state, 0, sizeof(u32) * 4, s);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&done, cudaEventDisableTiming);
+    if (e != cudaSuccess) {
+        cudaFree(owner);
+        cudaFree(lists);
+        cudaFree(lkeys);
+        cudaFree(state);
+        if (done) cudaEventDestroy(done);
+        return fail(e == cudaErrorMemoryAllocation ? BC_ENOMEM : BC_ECUDA,
+                    "ordered-insert scratch: %s", cudaGetErrorString(e));
+    }
+    f->d_lists = lists;
+    f->d_lkeys = lkeys;
+    f->d_state = state;
+    f->ord_done = done;
     f->chunk = chunk;
     f->slots = slots;
     f->owner_words = owner_words;
     f->rounds_bound = 0;
+    f->d_owner = owner;  // published last: the "scratch ready" flag
+    return BC_OK;
+}
+
+// Ordered launches on a handle run one at a time even from several streams:
+// the caller's stream first waits for the previous launch (its scratch), and
+// the launch is recorded as the new previous one.  Call with f->mu held.
+static int ordered_begin(bc_filter *f, cudaStream_t s) {
+    CUDA_TRY(cudaStreamWaitEvent(s, f->ord_done, 0));
+    return BC_OK;
+}
+
+static int ordered_end(bc_filter *f, cudaStream_t s) {
+    CUDA_TRY(cudaEventRecord(f->ord_done, s));
+    return BC_OK;
+}
+
+// Every round commits at least one key, so rounds <= keys: re-arm the round
+// tags long before the 32-bit counter could wrap.
+static int ordered_rearm(bc_filter *f, u64 n, cudaStream_t s) {
+    if (f->rounds_bound + n >= (1ull << 31)) {
+        CUDA_TRY(cudaMemsetAsync(f->d_owner, 0xff, sizeof(u64) * f->owner_words, s));
+        CUDA_TRY(cudaMemsetAsync(f->d_state, 0, sizeof(u32) * 4, s));
+        f->rounds_bound = 0;
+    }
     return BC_OK;
 }
 
@@ -367,21 +419,20 @@ static int insert_device(bc_filter *f, u64 *words, const u64 *keys, u64 n, int m
     }
     std::lock_guard<std::mutex> lk(f->mu);
     int rc = ensure_ordered_scratch(f, s);
+    if (rc == BC_OK) rc = ordered_begin(f, s);
     if (rc) return rc;
-    // every round commits at least one key, so rounds <= keys: re-arm the
-    // round tags long before the 32-bit counter could wrap
-    if (f->rounds_bound + n >= (1ull << 31)) {
-        CUDA_TRY(cudaMemsetAsync(f->d_owner, 0xff, sizeof(u64) * f->owner_words, s));
-        CUDA_TRY(cudaMemsetAsync(f->d_state, 0, sizeof(u32) * 4, s));
-        f->rounds_bound = 0;
-    }
-    for (u64 off = 0; off < n; off += (1ull << 30)) {
+    for (u64 off = 0; off < n && rc == BC_OK; off += (1ull << 30)) {
         const u64 len = std::min<u64>(1ull << 30, n - off);
-        CUDA_TRY(launch_ordered(f->kp, words, keys + off, len, f->chunk, f->d_owner, f->slots,
-                                f->d_lists, f->d_state, s));
+        rc = ordered_rearm(f, len, s);
+        if (rc) break;
+        cudaError_t e = launch_ordered(f->kp, words, keys + off, len, f->chunk, f->d_owner,
+                                       f->slots, f->d_lists, f->d_lkeys, f->d_state, s);
+        if (e != cudaSuccess)
+            rc = fail(BC_ECUDA, "ordered insert: %s", cudaGetErrorString(e));
         f->rounds_bound += len;
     }
-    return BC_OK;
+    const int rc2 = ordered_end(f, s);
+    return rc ? rc : rc2;
 }
 
 extern "C" int bc_insert(bc_filter *f, uint64_t *d_words, const uint64_t *d_keys, uint64_t n,
@@ -438,27 +489,57 @@ extern "C" int bc_encode_qgrams(const uint8_t *d_seq, uint64_t len, int q, int c
     return BC_OK;
 }
 
-// Materialise the keys (for the paths the fused kernel does not cover:
-// ordered c >= 2 inserts, standard filters, non-512-bit blocks).
-static int encode_tmp(const u8 *seq, u64 len, int q, int canonical, u64 rec, u64 **keys,
+// Materialise the keys of a window slice (for the geometries no fused kernel
+// covers: non-512-bit blocks, the distinct strategy with c >= 2, standard
+// filters).  The caller walks the sequence in slices of kEncodeSlice windows
+// (consecutive inserts equal one insert; lookups write at the running answer
+// offset), so at most kEncodeSlice keys are ever materialised.
+static constexpr u64 kEncodeSlice = 1ull << 26;
+
+static int encode_tmp(const u8 *seq, u64 len, int q, int canonical, RecSpec rec, u64 **keys,
                       u64 *n, cudaStream_t s) {
     const u64 nwin = qgram_windows(len, q);
     *keys = nullptr;
     *n = 0;
     if (nwin == 0) return BC_OK;
     unsigned long long *d_cnt = nullptr;
+    u64 *tiles = nullptr;
+    const u64 ntiles = (nwin + kQgramTile - 1) / kQgramTile;
     CUDA_TRY(cudaMallocAsync((void **)keys, sizeof(u64) * nwin, s));
-    CUDA_TRY(cudaMallocAsync((void **)&d_cnt, sizeof(*d_cnt), s));
-    int rc = bc_encode_qgrams(seq, len, q, canonical, rec, *keys, d_cnt, s);
+    cudaError_t e = cudaMallocAsync((void **)&d_cnt, sizeof(*d_cnt), s);
+    if (e == cudaSuccess) e = cudaMallocAsync((void **)&tiles, sizeof(u64) * ntiles, s);
+    if (e == cudaSuccess) e = launch_qgram_offsets(seq, len, q, rec, tiles, ntiles, d_cnt, s);
+    if (e == cudaSuccess) e = launch_qgram_encode(seq, len, q, canonical, rec, tiles, *keys, s);
     unsigned long long h_cnt = 0;
-    if (rc == BC_OK) {
-        cudaError_t e = cudaMemcpyAsync(&h_cnt, d_cnt, sizeof h_cnt, cudaMemcpyDeviceToHost, s);
-        if (e == cudaSuccess) e = cudaStreamSynchronize(s);
-        if (e != cudaSuccess) rc = fail(BC_ECUDA, "%s", cudaGetErrorString(e));
+    if (e == cudaSuccess)
+        e = cudaMemcpyAsync(&h_cnt, d_cnt, sizeof h_cnt, cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (tiles) cudaFreeAsync(tiles, s);
+    if (d_cnt) cudaFreeAsync(d_cnt, s);
+    if (e != cudaSuccess) {
+        cudaFreeAsync(*keys, s);
+        *keys = nullptr;
+        return fail(BC_ECUDA, "q-gram encode: %s", cudaGetErrorString(e));
     }
-    cudaFreeAsync(d_cnt, s);
     *n = h_cnt;
-    return rc;
+    return BC_OK;
+}
+
+// Record spec of the slice starting at window w of a sequence.
+static RecSpec slice_rec(u64 record_len, u64 w) {
+    return RecSpec{record_len, record_len ? w % record_len : 0};
+}
+
+static int add_count(unsigned long long *d_count, u64 n, cudaStream_t s) {
+    if (!d_count || n == 0) return BC_OK;
+    // d_count was zeroed on the stream; add the host-known total
+    unsigned long long hn = 0;
+    CUDA_TRY(cudaMemcpyAsync(&hn, d_count, sizeof hn, cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+    hn += n;
+    CUDA_TRY(cudaMemcpyAsync(d_count, &hn, sizeof hn, cudaMemcpyHostToDevice, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+    return BC_OK;
 }
 
 extern "C" int bc_insert_qgrams(bc_filter *f, uint64_t *d_words, const uint8_t *d_seq,
@@ -474,30 +555,53 @@ extern "C" int bc_insert_qgrams(bc_filter *f, uint64_t *d_words, const uint8_t *
     if (d_count) CUDA_TRY(cudaMemsetAsync(d_count, 0, sizeof(*d_count), s));
     if (nwin == 0) return BC_OK;
     if (!d_words || !d_seq) return fail(BC_EINVAL, "null words or sequence");
-    const bool fused = f->kind != BC_KIND_STANDARD && f->kp.wpb == 8 &&
-                       (f->kp.c == 1 || mode == BC_INSERT_RELAXED);
-    if (fused) {
-        // c == 1: one launch.  relaxed: windows in slices of M/2.
+    const bool blocks512 = f->kind != BC_KIND_STANDARD && f->kp.wpb == 8;
+    if (blocks512 && (f->kp.c == 1 || mode == BC_INSERT_RELAXED)) {
+        // c == 1: one launch (OR commutes).  relaxed: windows in slices of M/2.
         const u64 per = f->kp.c == 1 ? nwin : std::max<u64>(1, f->kp.num_blocks / 2);
         for (u64 w = 0; w < nwin; w += per) {
             const u64 nw = std::min(per, nwin - w);
-            const RecSpec rec{record_len, record_len ? w % record_len : 0};
             CUDA_TRY(launch_qgram_blocks(OP_INSERT, f->kp, d_words, d_seq + w, nw + q - 1, q,
-                                         canonical, rec, nullptr, nullptr, nullptr, d_count, s));
+                                         canonical, slice_rec(record_len, w), nullptr, nullptr,
+                                         nullptr, d_count, s));
         }
         return BC_OK;
     }
-    u64 *keys = nullptr, n = 0;
-    int rc = encode_tmp(d_seq, len, q, canonical, record_len, &keys, &n, s);
-    if (rc == BC_OK) rc = insert_device(f, d_words, keys, n, mode, s);
-    if (rc == BC_OK && d_count) {
-        unsigned long long hn = n;
-        cudaError_t e = cudaMemcpyAsync(d_count, &hn, sizeof hn, cudaMemcpyHostToDevice, s);
-        if (e == cudaSuccess) e = cudaStreamSynchronize(s);
-        if (e != cudaSuccess) rc = fail(BC_ECUDA, "%s", cudaGetErrorString(e));
+    if (blocks512 && ordered_tiles_supported(f->kp)) {
+        // exact stream order, keys encoded on the fly from the sequence
+        // (window index = priority): no key array
+        std::lock_guard<std::mutex> lk(f->mu);
+        int rc = ensure_ordered_scratch(f, s);
+        if (rc == BC_OK) rc = ordered_begin(f, s);
+        if (rc) return rc;
+        for (u64 w = 0; w < nwin && rc == BC_OK; w += (1ull << 30)) {
+            const u64 nw = std::min<u64>(1ull << 30, nwin - w);
+            rc = ordered_rearm(f, nw, s);
+            if (rc) break;
+            cudaError_t e = launch_ordered_qgrams(f->kp, d_words, d_seq + w, nw, q, canonical,
+                                                  slice_rec(record_len, w), f->chunk, f->d_owner,
+                                                  f->slots, f->d_lists, f->d_lkeys, f->d_state,
+                                                  d_count, s);
+            if (e != cudaSuccess)
+                rc = fail(BC_ECUDA, "ordered q-gram insert: %s", cudaGetErrorString(e));
+            f->rounds_bound += nw;
+        }
+        const int rc2 = ordered_end(f, s);
+        return rc ? rc : rc2;
     }
-    if (keys) cudaFreeAsync(keys, s);
-    return rc;
+    // other geometries: bounded slices of materialised keys
+    u64 total = 0;
+    for (u64 w = 0; w < nwin; w += kEncodeSlice) {
+        const u64 nw = std::min(kEncodeSlice, nwin - w);
+        u64 *keys = nullptr, n = 0;
+        int rc = encode_tmp(d_seq + w, nw + q - 1, q, canonical, slice_rec(record_len, w), &keys,
+                            &n, s);
+        if (rc == BC_OK) rc = insert_device(f, d_words, keys, n, mode, s);
+        if (keys) cudaFreeAsync(keys, s);
+        if (rc) return rc;
+        total += n;
+    }
+    return add_count(d_count, total, s);
 }
 
 extern "C" int bc_contains_qgrams(bc_filter *f, const uint64_t *d_words, const uint8_t *d_seq,
@@ -534,17 +638,20 @@ extern "C" int bc_contains_qgrams(bc_filter *f, const uint64_t *d_words, const u
         CUDA_TRY(e);
         return BC_OK;
     }
-    u64 *keys = nullptr, n = 0;
-    int rc = encode_tmp(d_seq, len, q, canonical, record_len, &keys, &n, s);
-    if (rc == BC_OK) rc = contains_device(f, d_words, keys, n, d_out, d_hits, s);
-    if (rc == BC_OK && d_count) {
-        unsigned long long hn = n;
-        cudaError_t e = cudaMemcpyAsync(d_count, &hn, sizeof hn, cudaMemcpyHostToDevice, s);
-        if (e == cudaSuccess) e = cudaStreamSynchronize(s);
-        if (e != cudaSuccess) rc = fail(BC_ECUDA, "%s", cudaGetErrorString(e));
+    if (d_count) CUDA_TRY(cudaMemsetAsync(d_count, 0, sizeof(*d_count), s));
+    u64 total = 0;
+    for (u64 w = 0; w < nwin; w += kEncodeSlice) {
+        const u64 nw = std::min(kEncodeSlice, nwin - w);
+        u64 *keys = nullptr, n = 0;
+        int rc = encode_tmp(d_seq + w, nw + q - 1, q, canonical, slice_rec(record_len, w), &keys,
+                            &n, s);
+        if (rc == BC_OK)
+            rc = contains_device(f, d_words, keys, n, d_out ? d_out + total : nullptr, d_hits, s);
+        if (keys) cudaFreeAsync(keys, s);
+        if (rc) return rc;
+        total += n;
     }
-    if (keys) cudaFreeAsync(keys, s);
-    return rc;
+    return add_count(d_count, total, s);
 }
 
 // ---- analysis / routing ---------------------------------------------------------------

@@ -8,10 +8,11 @@
 //                            tile's hashing overlapped with the loads
 //   lookup512_kernel<C, K>   lookups: staged blocks, early exit over choices
 //   lookup512_pipe_kernel<K> single-choice lookups, two tiles in flight
-//   ordered512_kernel<C>     exact stream-order insert for c >= 2, 512-bit
+//   ordered512_kernel<C,Src> exact stream-order insert for c >= 2, 512-bit
 //                            blocks: claim rounds over a sliding window, one
 //                            cooperative launch, winners committed a warp
-//                            tile at a time
+//                            tile at a time; keys from an array or encoded
+//                            from a DNA sequence on the fly (keysrc.cuh)
 //   ordered_window_kernel    the same rounds for any geometry, thread-per-key
 //                            commits (ordered_kernel: fixed-chunk variant)
 //   flat_kernel<OP>          standard Bloom filter (k global bits)
@@ -24,6 +25,7 @@
 #include <unordered_map>
 
 #include "blocks.cuh"
+#include "keysrc.cuh"
 #include "lookup.cuh"
 
 namespace cg = cooperative_groups;
@@ -534,11 +536,11 @@ __global__ void __launch_bounds__(256) ordered_window_kernel(
 #ifndef BC_ORD_MINB
 #define BC_ORD_MINB 3  // <= 80 registers: 3 CTAs per SM (cfg3 +4%, cfg5 +8% over 2 CTAs at 102)
 #endif
-template <int C>
+template <int C, class Src>
 __global__ void __launch_bounds__(kTPB, BC_ORD_MINB) ordered512_kernel(
-    const __grid_constant__ KParams p, u64 *__restrict__ words, const u64 *__restrict__ keys,
-    u64 n, u64 window, u32 *__restrict__ owner, u64 slots, u32 slot_shift,
-    u32 *__restrict__ lists, u32 *__restrict__ state) {
+    const __grid_constant__ KParams p, u64 *__restrict__ words, const Src src, u64 n, u64 window,
+    u32 *__restrict__ owner, u64 slots, u32 slot_shift, u32 *__restrict__ lists,
+    u64 *__restrict__ lkeys, u32 *__restrict__ state, unsigned long long *__restrict__ admitted) {
     cg::grid_group grid = cg::this_grid();
     __shared__ WarpSmem<C> smem[kWarps];
     WarpSmem<C> &ws = smem[threadIdx.x >> 5];
@@ -546,8 +548,12 @@ __global__ void __launch_bounds__(kTPB, BC_ORD_MINB) ordered512_kernel(
     const u64 warp = blockIdx.x * (u64)kWarps + (threadIdx.x >> 5);
     const u64 wstride = (u64)gridDim.x * kTPB;
     u32 round = __ldcg(state);
+    // pending lists: the key's stream index (its priority) and the key itself,
+    // so a key that loses a round is neither re-read nor re-derived
     u32 *cur = lists, *nxt = lists + window;
+    u64 *curk = lkeys, *nxtk = lkeys + window;
     u64 npend = 0, next = 0;
+    u32 n_admitted = 0;
     while (npend > 0 || next < n) {
         const u64 admit = min(window - npend, n - next);
         u32 *own_cur = owner + (round & 1u) * slots;
@@ -555,19 +561,29 @@ __global__ void __launch_bounds__(kTPB, BC_ORD_MINB) ordered512_kernel(
         u32 *cnt = state + 1 + round % 3u;
         if (warp == 0 && lane == 0) state[1 + (round + 1u) % 3u] = 0;
         const u64 total = npend + admit;
-        // warp-uniform tiles; the next tile's list entry and key are loaded
-        // while the current tile's candidate blocks are read and committed
+        // tile entry t: a pending key from the list, or the next key of the
+        // stream (admit() is false for an index without a key)
+        auto fetch = [&](u64 t, u32 &li, u64 &x) -> bool {
+            if (t >= total) return false;
+            if (t < npend) {
+                li = __ldcg(cur + t);
+                x = __ldcg(curk + t);
+                return true;
+            }
+            const u64 idx = next + (t - npend);
+            li = (u32)idx;
+            const bool ok = src.admit(idx, x);
+            n_admitted += ok ? 1u : 0u;
+            return ok;
+        };
+        // warp-uniform tiles; the next tile's entries are fetched while the
+        // current tile's candidate blocks are read and committed
         u64 t0 = warp * 32;
         u32 li = 0;
         u64 x = 0;
-        if (t0 + lane < total) {
-            const u64 t = t0 + lane;
-            li = t < npend ? __ldcg(cur + t) : (u32)(next + (t - npend));
-            x = keys[li];
-        }
+        bool valid = fetch(t0 + lane, li, x);
         while (t0 < total) {
             const u64 t = t0 + lane;
-            const bool valid = t < total;
             const bool win = valid && t < npend && ordered_check(p, own_cur, slot_shift, x, li);
             const bool lose = valid && !win;
             if (lose) ordered_claim(p, own_nxt, slot_shift, x, li);
@@ -578,11 +594,7 @@ __global__ void __launch_bounds__(kTPB, BC_ORD_MINB) ordered512_kernel(
             const u64 t1 = t0 + wstride;
             u32 li_n = 0;
             u64 x_n = 0;
-            if (t1 + lane < total) {
-                const u64 tn = t1 + lane;
-                li_n = tn < npend ? __ldcg(cur + tn) : (u32)(next + (tn - npend));
-                x_n = keys[li_n];
-            }
+            const bool valid_n = fetch(t1 + lane, li_n, x_n);
             if (__ballot_sync(kFull, win)) {  // tiles of admitted keys only claim
                 phase1<C>(p, x, win, ws, lane);
                 __syncwarp();
@@ -591,10 +603,15 @@ __global__ void __launch_bounds__(kTPB, BC_ORD_MINB) ordered512_kernel(
             }
             if (lm) {
                 base = __shfl_sync(kFull, base, 0);
-                if (lose) nxt[base + __popc(lm & ((1u << lane) - 1u))] = li;
+                if (lose) {
+                    const u32 slot = base + __popc(lm & ((1u << lane) - 1u));
+                    nxt[slot] = li;
+                    nxtk[slot] = x;
+                }
             }
             li = li_n;
             x = x_n;
+            valid = valid_n;
             t0 = t1;
         }
         grid.sync();
@@ -603,7 +620,14 @@ __global__ void __launch_bounds__(kTPB, BC_ORD_MINB) ordered512_kernel(
         u32 *tmp = cur;
         cur = nxt;
         nxt = tmp;
+        u64 *tmpk = curk;
+        curk = nxtk;
+        nxtk = tmpk;
         ++round;
+    }
+    if (Src::kCounts && admitted != nullptr) {
+        for (int o = 16; o > 0; o >>= 1) n_admitted += __shfl_xor_sync(kFull, n_admitted, o);
+        if (lane == 0 && n_admitted) atomicAdd(admitted, (unsigned long long)n_admitted);
     }
     if (warp == 0 && lane == 0) state[0] = round;
 }
@@ -961,15 +985,16 @@ static bool ordered_tiles() {
     return on;
 }
 
+template <class Src>
 static const void *ordered512_ptr(u32 c) {
     switch (c) {
-        case 2: return (const void *)ordered512_kernel<2>;
-        case 3: return (const void *)ordered512_kernel<3>;
-        case 4: return (const void *)ordered512_kernel<4>;
-        case 5: return (const void *)ordered512_kernel<5>;
-        case 6: return (const void *)ordered512_kernel<6>;
-        case 7: return (const void *)ordered512_kernel<7>;
-        default: return (const void *)ordered512_kernel<8>;
+        case 2: return (const void *)ordered512_kernel<2, Src>;
+        case 3: return (const void *)ordered512_kernel<3, Src>;
+        case 4: return (const void *)ordered512_kernel<4, Src>;
+        case 5: return (const void *)ordered512_kernel<5, Src>;
+        case 6: return (const void *)ordered512_kernel<6, Src>;
+        case 7: return (const void *)ordered512_kernel<7, Src>;
+        default: return (const void *)ordered512_kernel<8, Src>;
     }
 }
 
@@ -979,58 +1004,75 @@ u64 ordered_owner_words(u64 num_blocks, u64 slots) {
     return ordered_window_mode() ? slots : num_blocks;
 }
 
+bool ordered_tiles_supported(const KParams &p) {
+    return p.fast_random && p.wpb == 8 && p.c >= 2 && p.c <= 8 && ordered_tiles();
+}
+
+// Cooperative launch of the sliding-window kernel: the claim arrays (not the
+// filter: ordered builds run on filters of any size) persist in L2 when they
+// fit, since every pending key reads and claims c random slots per round.
+template <class Src>
+static cudaError_t launch_window(const KParams &p, u64 *words, const Src *src, const u64 *keys,
+                                 u64 n, u64 chunk, u64 *owner, u64 slots, u32 *lists, u64 *lkeys,
+                                 u32 *state, unsigned long long *admitted, cudaStream_t s) {
+    if (chunk == 0) return cudaErrorInvalidValue;  // no window: the rounds could never admit
+    // the append counters state[1..3] start at zero, the round counter
+    // state[0] (array parity) carries over
+    cudaError_t e = cudaMemsetAsync(state + 1, 0, 3 * sizeof(u32), s);
+    if (e != cudaSuccess) return e;
+    const bool tile = src != nullptr;
+    const void *fw = tile ? ordered512_ptr<Src>(p.c) : (const void *)ordered_window_kernel;
+    const unsigned grid = grid_for(fw, 256, 0, (chunk + 255) / 256);
+    u32 slot_shift = 0;  // identity slots when there is one per block
+    if (slots < p.num_blocks) slot_shift = 64u - (u32)__builtin_ctzll(slots);
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(256);
+    cfg.stream = s;
+    cudaLaunchAttribute attr[2];
+    attr[0].id = cudaLaunchAttributeCooperative;
+    attr[0].val.cooperative = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    size_t bytes = 0;
+    float hit = 0.f;
+    const size_t claim_bytes = sizeof(u32) * 2 * slots;
+    if (l2_window(claim_bytes, &bytes, &hit)) {
+        attr[1].id = cudaLaunchAttributeAccessPolicyWindow;
+        attr[1].val.accessPolicyWindow.base_ptr = owner;
+        attr[1].val.accessPolicyWindow.num_bytes = bytes;
+        attr[1].val.accessPolicyWindow.hitRatio = hit;
+        attr[1].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+        attr[1].val.accessPolicyWindow.missProp = cudaAccessPropertyNormal;
+        cfg.numAttrs = 2;
+    }
+    count_launch();
+    u32 *own = reinterpret_cast<u32 *>(owner);
+    if (!tile)
+        return cudaLaunchKernelEx(&cfg, ordered_window_kernel, p, words, keys, n, chunk, own,
+                                  slots, slot_shift, lists, state);
+    switch (p.c) {
+#define BC_ORD_C(c)                                                                         \
+    case c:                                                                                 \
+        return cudaLaunchKernelEx(&cfg, ordered512_kernel<c, Src>, p, words, *src, n, chunk, \
+                                  own, slots, slot_shift, lists, lkeys, state, admitted);
+        BC_ORD_C(2) BC_ORD_C(3) BC_ORD_C(4) BC_ORD_C(5) BC_ORD_C(6) BC_ORD_C(7) BC_ORD_C(8)
+#undef BC_ORD_C
+    }
+    return cudaErrorInvalidValue;
+}
+
 cudaError_t launch_ordered(const KParams &p, u64 *words, const u64 *keys, u64 n, u64 chunk,
-                           u64 *owner, u64 slots, u32 *lists, u32 *state, cudaStream_t s) {
+                           u64 *owner, u64 slots, u32 *lists, u64 *lkeys, u32 *state,
+                           cudaStream_t s) {
     if (n == 0) return cudaSuccess;
     if (ordered_window_mode()) {
-        // the append counters state[1..3] start at zero, the round counter
-        // state[0] (array parity) carries over
-        cudaError_t e = cudaMemsetAsync(state + 1, 0, 3 * sizeof(u32), s);
-        if (e != cudaSuccess) return e;
-        const bool tile = p.fast_random && p.wpb == 8 && p.c >= 2 && p.c <= 8 && ordered_tiles();
-        const void *fw = tile ? ordered512_ptr(p.c) : (const void *)ordered_window_kernel;
-        const unsigned grid = grid_for(fw, 256, 0, (chunk + 255) / 256);
-        u32 slot_shift = 0;  // identity slots when there is one per block
-        if (slots < p.num_blocks) slot_shift = 64u - (u32)__builtin_ctzll(slots);
-        cudaLaunchConfig_t cfg{};
-        cfg.gridDim = dim3(grid);
-        cfg.blockDim = dim3(256);
-        cfg.stream = s;
-        cudaLaunchAttribute attr[2];
-        attr[0].id = cudaLaunchAttributeCooperative;
-        attr[0].val.cooperative = 1;
-        cfg.attrs = attr;
-        cfg.numAttrs = 1;
-        // the claim arrays (not the filter: ordered builds run on filters of
-        // any size) persist in L2 when they fit: every pending key reads and
-        // claims c random slots per round
-        size_t bytes = 0;
-        float hit = 0.f;
-        const size_t claim_bytes = sizeof(u32) * 2 * slots;
-        if (l2_window(claim_bytes, &bytes, &hit)) {
-            attr[1].id = cudaLaunchAttributeAccessPolicyWindow;
-            attr[1].val.accessPolicyWindow.base_ptr = owner;
-            attr[1].val.accessPolicyWindow.num_bytes = bytes;
-            attr[1].val.accessPolicyWindow.hitRatio = hit;
-            attr[1].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
-            attr[1].val.accessPolicyWindow.missProp = cudaAccessPropertyNormal;
-            cfg.numAttrs = 2;
-        }
-        count_launch();
-        u32 *own = reinterpret_cast<u32 *>(owner);
-        if (!tile)
-            return cudaLaunchKernelEx(&cfg, ordered_window_kernel, p, words, keys, n, chunk, own,
-                                      slots, slot_shift, lists, state);
-        switch (p.c) {
-#define BC_ORD_C(c)                                                                          \
-    case c:                                                                                  \
-        return cudaLaunchKernelEx(&cfg, ordered512_kernel<c>, p, words, keys, n, chunk, own, \
-                                  slots, slot_shift, lists, state);
-            BC_ORD_C(2) BC_ORD_C(3) BC_ORD_C(4) BC_ORD_C(5) BC_ORD_C(6) BC_ORD_C(7) BC_ORD_C(8)
-#undef BC_ORD_C
-        }
-        return cudaErrorInvalidValue;
+        const ArrayKeys src{keys};
+        return launch_window<ArrayKeys>(p, words, ordered_tiles_supported(p) ? &src : nullptr,
+                                        keys, n, chunk, owner, slots, lists, lkeys, state,
+                                        nullptr, s);
     }
+    if (chunk == 0) return cudaErrorInvalidValue;
     l2_release();
     const void *fn = (const void *)ordered_kernel;
     const unsigned grid = grid_for(fn, 256, 0, (chunk + 255) / 256);
@@ -1040,6 +1082,22 @@ cudaError_t launch_ordered(const KParams &p, u64 *words, const u64 *keys, u64 n,
     cudaError_t e = cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(256), args, 0, s);
     count_launch();
     return e;
+}
+
+cudaError_t launch_ordered_qgrams(const KParams &p, u64 *words, const u8 *seq, u64 nwin, int q,
+                                  int canonical, RecSpec rec, u64 chunk, u64 *owner, u64 slots,
+                                  u32 *lists, u64 *lkeys, u32 *state,
+                                  unsigned long long *count, cudaStream_t s) {
+    if (nwin == 0) return cudaSuccess;
+    if (!ordered_window_mode() || !ordered_tiles_supported(p)) return cudaErrorInvalidValue;
+    SeqKeys src;
+    src.seq = seq;
+    src.rec = rec;
+    src.q = (u32)q;
+    src.canonical = (u32)canonical;
+    src.qmask = q == 32 ? ~0ull : ((1ull << (2 * q)) - 1ull);
+    return launch_window<SeqKeys>(p, words, &src, nullptr, nwin, chunk, owner, slots, lists,
+                                  lkeys, state, count, s);
 }
 
 cudaError_t launch_flat(int op, const KParams &p, u64 *words, const u64 *keys, u64 n, u8 *out,

@@ -31,10 +31,14 @@ cudaError_t launch_blocks(int op, const KParams &p, u64 *words, const u64 *keys,
 // owner: the claim arrays, ordered_owner_words(num_blocks, slots) u64 words,
 // all-ones before the first launch (slots == num_blocks: one per block, else
 // a power of two, blocks hashed onto slots).  n < 2^32 - 1 per launch.
+// lists: 2 * chunk u32 stream indices; lkeys: 2 * chunk u64 keys (the
+// pending lists of the tiled kernel).  chunk == 0 is rejected.
 bool ordered_window_mode();
+bool ordered_tiles_supported(const KParams &p);
 u64 ordered_owner_words(u64 num_blocks, u64 slots);
 cudaError_t launch_ordered(const KParams &p, u64 *words, const u64 *keys, u64 n, u64 chunk,
-                           u64 *owner, u64 slots, u32 *lists, u32 *state, cudaStream_t s);
+                           u64 *owner, u64 slots, u32 *lists, u64 *lkeys, u32 *state,
+                           cudaStream_t s);
 
 // ---- standard (flat) kind --------------------------------------------------------
 cudaError_t launch_flat(int op, const KParams &p, u64 *words, const u64 *keys, u64 n, u8 *out,
@@ -66,6 +70,15 @@ cudaError_t launch_qgram_blocks(int op, const KParams &p, u64 *words, const u8 *
                                 int q, int canonical, RecSpec rec, const u64 *tile_off, u8 *out,
                                 unsigned long long *hits, unsigned long long *count,
                                 cudaStream_t s);
+
+// Exact stream-order insert of the q-gram windows of seq (nwin windows, i.e.
+// seq holds nwin + q - 1 bytes): == launch_ordered on encode_qgrams(seq),
+// keys encoded on the fly (keysrc.cuh), window index = stream priority.
+// Needs ordered_tiles_supported(p).  *count += windows inserted (valid ones).
+cudaError_t launch_ordered_qgrams(const KParams &p, u64 *words, const u8 *seq, u64 nwin, int q,
+                                  int canonical, RecSpec rec, u64 chunk, u64 *owner, u64 slots,
+                                  u32 *lists, u64 *lkeys, u32 *state,
+                                  unsigned long long *count, cudaStream_t s);
 
 // numpy PCG64 stream (default_rng(seed).integers(0, 2**64, uint64)) from a
 // seeded (state, inc): outputs [offset, offset+n), then & and_mask | or_mask.

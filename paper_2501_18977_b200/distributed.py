@@ -162,24 +162,34 @@ def _peer_mode() -> int:
     return -1 if v is None else int(v)
 
 
-_PEER_CACHE: dict = {}  # (group, ptr, numel) -> PeerReplicas or None
-_IPC_OPEN: dict = {}    # exported allocation handle -> its base address here
+# (id(group), ptr, numel) -> PeerReplicas (successful mappings only).  An
+# entry holds no reference to the replica tensor (an 8 GiB filter must not be
+# kept alive by a cache); whether it may be reused is decided collectively
+# and re-validated against the allocation's current IPC handle (see
+# _peer_replicas).
+_PEER_CACHE: dict = {}
+_IPC_OPEN: dict = {}  # peer allocation handle -> [base address here, users]
 
 
 class PeerReplicas:
     """The ranks' replicas of one word tensor, mapped into this process
     (CUDA IPC; lazy peer access over NVLink)."""
 
-    def __init__(self, words: torch.Tensor, rank: int, ptrs: list):
+    def __init__(self, words: torch.Tensor, rank: int, ptrs: list, own: tuple, peers: list):
         self.world, self.rank, self.nwords = len(ptrs), rank, words.numel()
         self.ptrs = (ctypes.c_uint64 * len(ptrs))(*ptrs)
-        self.words = words  # keeps the local replica (and its mapping) alive
+        self.own = own        # this rank's (handle, offset) when the mapping was made
+        self.peers = peers    # imported handles (released in close())
 
     def or_allreduce(self, stream) -> None:
         from . import _native
 
         _native.check(_native.lib().bc_or_allreduce_peers(
             self.ptrs, self.world, self.rank, self.nwords, ctypes.c_void_p(stream)))
+
+    def close(self) -> None:
+        _release(self.peers)
+        self.peers = []
 
 
 def _export(words: torch.Tensor):
@@ -196,11 +206,29 @@ def _export(words: torch.Tensor):
         return None
 
 
-def _import(infos: list, rank: int, words: torch.Tensor):
-    """This process's addresses of every rank's replica, or None."""
+def _release(handles: list) -> None:
+    """Drop one use of each imported peer allocation; unmap at zero."""
     from . import _native
 
-    ptrs = []
+    for h in handles:
+        ent = _IPC_OPEN.get(h)
+        if ent is None:
+            continue
+        ent[1] -= 1
+        if ent[1] <= 0:
+            del _IPC_OPEN[h]
+            try:
+                _native.check(_native.lib().bc_ipc_close(ctypes.c_void_p(ent[0]), 0))
+            except (RuntimeError, ValueError):
+                pass
+
+
+def _import(infos: list, rank: int, words: torch.Tensor):
+    """(this process's addresses of every rank's replica, imported handles),
+    or None."""
+    from . import _native
+
+    ptrs, used = [], []
     try:
         for j, (h, o) in enumerate(infos):
             if j == rank:
@@ -209,25 +237,30 @@ def _import(infos: list, rank: int, words: torch.Tensor):
             if h not in _IPC_OPEN:
                 base = ctypes.c_void_p()
                 _native.check(_native.lib().bc_ipc_import(h, 0, ctypes.byref(base)))
-                _IPC_OPEN[h] = base.value
-            ptrs.append(_IPC_OPEN[h] + o)
+                _IPC_OPEN[h] = [base.value, 0]
+            _IPC_OPEN[h][1] += 1
+            used.append(h)
+            ptrs.append(_IPC_OPEN[h][0] + o)
     except (RuntimeError, ValueError, MemoryError):
+        _release(used)
         return None
-    return ptrs
+    return ptrs, used
 
 
 def _peer_replicas(words: torch.Tensor, group):
-    """Cached PeerReplicas when every rank can map every other rank's
-    replica, else None.  Every rank runs the same collectives in the same
-    order whatever fails locally, and the decision is the AND over ranks."""
+    """PeerReplicas when every rank can map every other rank's replica, else
+    None.  Every rank runs the same collectives in the same order whatever
+    fails locally, and every decision is the AND over ranks: a cached mapping
+    is reused only if, on every rank, it exists and this replica still lives
+    in the allocation (IPC handle and offset) the mapping was made for --
+    address reuse after a free, on some ranks only, therefore rebuilds the
+    mapping on all of them instead of splitting the ranks between two code
+    paths."""
     mode = _peer_mode()
     if mode == 0 or not words.is_cuda or not words.is_contiguous():
         return None
     if mode != 1 and dist.get_backend(group) != "nccl":
         return None
-    key = (id(group), words.data_ptr(), words.numel())
-    if key in _PEER_CACHE:
-        return _PEER_CACHE[key]
     rank, world = _rank_world(group)
 
     def agree(local):
@@ -235,17 +268,27 @@ def _peer_replicas(words: torch.Tensor, group):
         dist.all_gather_object(out, local, group=group)
         return out
 
+    key = (id(group), words.data_ptr(), words.numel())
+    own = _export(words)
+    cached = _PEER_CACHE.get(key)
+    if all(agree(cached is not None and own is not None and cached.own == own)):
+        return cached
+    if cached is not None:
+        cached.close()
+        del _PEER_CACHE[key]
     dev = words.device.index
     devs = agree(dev)
-    ok = words.data_ptr() % 16 == 0 and world <= 16 and all(
+    ok = own is not None and words.data_ptr() % 16 == 0 and world <= 16 and all(
         d == dev or torch.cuda.can_device_access_peer(dev, d) for d in devs)
-    reps = None
-    if all(agree(bool(ok))):
-        infos = agree(_export(words))
-        if all(i is not None for i in infos):
-            ptrs = _import(infos, rank, words)
-            if all(agree(ptrs is not None)):
-                reps = PeerReplicas(words, rank, ptrs)
+    if not all(agree(bool(ok))):
+        return None
+    infos = agree(own)
+    imp = _import(infos, rank, words)
+    if not all(agree(imp is not None)):
+        if imp is not None:
+            _release(imp[1])
+        return None
+    reps = PeerReplicas(words, rank, imp[0], own, imp[1])
     _PEER_CACHE[key] = reps
     return reps
 

@@ -67,7 +67,7 @@ def write_filter(filt: Filter, path) -> None:
     with open(path, "wb") as fh:
         fh.write(header)
         if st._d_words is None or st._host_valid:
-            fh.write(np.ascontiguousarray(st.words, dtype="<u8").tobytes())
+            fh.write(np.ascontiguousarray(st.words_readonly(), dtype="<u8").tobytes())
             return
         d = st.d_words
         for a in range(0, st.num_words, _SLICE_WORDS):

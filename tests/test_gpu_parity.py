@@ -86,42 +86,38 @@ def test_device_tensor_inputs(golden, name):
 @pytest.mark.parametrize("name", ["cfg1", "bc3_k12_20k", "bc2_k6_t4", "bc3_dist_k10",
                                   "bc8_k5", "bc2_b1024", "cfg3_small", "cfg5_small_k11"])
 def test_relaxed_build_tolerance(golden, name):
-    """Relaxed multi-choice inserts: zero false negatives, lookups of the
-    reference-built array unaffected, FPR and load histogram within the
-    stated tolerance."""
+    """Relaxed multi-choice inserts against the exact-order build of the same
+    stream (itself pinned to the reference's words), with SURVEY §8(a)'s
+    tolerances written here: zero false negatives; |log2 FPR_relaxed -
+    log2 FPR_exact| <= 0.1 + 3 sigma over 2^24 device-generated negatives;
+    mean block load within 1 bit; load variance within 15% (plus 3 sigma of
+    the variance estimate over the filter's M blocks); and, for filters
+    of at least 2^15 blocks (config 1 and up, where the tolerance is stated),
+    the unbinned load-histogram total variation <= 0.05."""
+    import math
+
     meta, _ = golden
     case = meta[name]
+    keys, _ = probes_of(case)
+    exact = bb.Filter.from_config(config_of(case))
+    exact.insert_many(keys)
+    assert sha(exact.storage.words) == case["words_sha256"]
     f = bb.Filter.from_config(config_of(case), insert_mode="relaxed")
-    keys, probes = probes_of(case)
     f.insert_many(keys)
     assert f.contains_many(keys).all()
-    neg = probes[case["hits_pos"]:]
-    hits = f.count_hits(neg)
-    ref = case["hits_neg"]
-    # false positives within 10% (|log2 FPR ratio| <~ 0.14) plus 4 sigma of the
-    # Poisson noise of both counts (relaxed builds are timing-dependent; 4
-    # sigma keeps the eight cases from flaking together)
-    assert abs(hits - ref) <= 0.1 * ref + 4 * np.sqrt(2.0 * max(ref, 1)) + 1, (hits, ref)
-    hist = bb.block_load_histogram(f)
-    assert abs(hist.mean_load - case["mean_load"]) <= max(1.0, 0.01 * case["mean_load"]), \
-        (hist.mean_load, case["mean_load"])
-    assert abs(hist.variance / case["variance"] - 1) <= 0.15 + 0.3 * (f.num_blocks < 1000), \
-        (hist.variance, case["variance"], f.num_blocks)
-    if f.num_blocks >= 4096:
-        # load-histogram total variation vs the exact build (SURVEY §8(a): <= 0.05)
-        exact = bb.Filter.from_config(config_of(case))
-        exact.insert_many(keys)
-        assert sha(exact.storage.words) == case["words_sha256"]
-        a, b = hist.counts, bb.block_load_histogram(exact).counts
-        if f.num_blocks < 1 << 16:
-            # below 2^16 blocks the per-load-value sampling noise alone comes
-            # near 0.05 (max of 10 relaxed builds, tools/relaxed_spread_probe.py:
-            # 0.054 at 8192 blocks, 0.042 at 32768), so compare the shapes on
-            # loads binned by 4
-            w = 4
-            a = np.add.reduceat(a, np.arange(0, len(a), w))
-            b = np.add.reduceat(b, np.arange(0, len(b), w))
-        tv = bb.histogram_distance(a, b)
+    neg = bb.odd_keys(1 << 24, 12, device="cuda")
+    fp_e, fp_r = exact.count_hits(neg), f.count_hits(neg)
+    sigma = math.sqrt(1 / max(fp_e, 1) + 1 / max(fp_r, 1)) / math.log(2)
+    assert abs(math.log2(max(fp_r, 1) / max(fp_e, 1))) <= 0.1 + 3 * sigma, (fp_e, fp_r)
+    h_r, h_e = bb.block_load_histogram(f), bb.block_load_histogram(exact)
+    assert abs(h_r.mean_load - h_e.mean_load) <= 1.0, (h_r.mean_load, h_e.mean_load)
+    # 15% plus 3 sigma of the variance estimate itself over M blocks
+    # (sqrt(2 / M) relative): a 57-block filter's variance is not resolvable
+    # to 15%, a config-1 filter's (2^15 blocks) is to within 2.3 points
+    tol = 0.15 + 3 * math.sqrt(2.0 / f.num_blocks)
+    assert abs(h_r.variance / h_e.variance - 1) <= tol, (h_r.variance, h_e.variance, tol)
+    if f.num_blocks >= 1 << 15:
+        tv = bb.histogram_distance(h_r.counts, h_e.counts)
         assert tv <= 0.05, tv
 
 
