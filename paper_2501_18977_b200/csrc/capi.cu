@@ -261,12 +261,31 @@ extern "C" void bc_filter_destroy(bc_filter *f) {
     delete f;
 }
 
+// The library's stream-ordered scratch (cudaMallocAsync: q-gram tile offsets,
+// hit counters, ticket arrays) comes from the device's default pool, whose
+// release threshold is 0: every synchronisation would hand the memory back
+// to the driver and the next call would map it again (~ms for tens of MB).
+// Keep up to 1 GiB of it reserved instead.
+static void keep_pool(int dev) {
+    static std::once_flag once[64];
+    if (dev < 0 || dev >= 64) return;
+    std::call_once(once[dev], [dev] {
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+            u64 keep = 1ull << 30;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+        }
+        cudaGetLastError();
+    });
+}
+
 static int check_device(bc_filter *f) {
     int dev = -1;
     cudaGetDevice(&dev);
     if (dev != f->device)
         return fail(BC_EINVAL, "filter handle belongs to device %d, current device is %d",
                     f->device, dev);
+    keep_pool(dev);
     return BC_OK;
 }
 
@@ -313,9 +332,9 @@ static int ensure_ordered_scratch(bc_filter *f, cudaStream_t s) {
     cudaError_t e = cudaMalloc(&owner, sizeof(u64) * owner_words);
     if (e == cudaSuccess) e = cudaMalloc(&lists, sizeof(u32) * 2 * chunk);
     if (e == cudaSuccess) e = cudaMalloc(&lkeys, sizeof(u64) * 2 * chunk);
-    if (e == cudaSuccess) e = cudaMalloc(&state, sizeof(u32) * 4);
+    if (e == cudaSuccess) e = cudaMalloc(&state, sizeof(u32) * 8);
     if (e == cudaSuccess) e = cudaMemsetAsync(owner, 0xff, sizeof(u64) * owner_words, s);
-    if (e == cudaSuccess) e = cudaMemsetAsync(state, 0, sizeof(u32) * 4, s);
+    if (e == cudaSuccess) e = cudaMemsetAsync(state, 0, sizeof(u32) * 8, s);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&done, cudaEventDisableTiming);
     if (e != cudaSuccess) {
         cudaFree(owner);
@@ -356,7 +375,7 @@ static int ordered_end(bc_filter *f, cudaStream_t s) {
 static int ordered_rearm(bc_filter *f, u64 n, cudaStream_t s) {
     if (f->rounds_bound + n >= (1ull << 31)) {
         CUDA_TRY(cudaMemsetAsync(f->d_owner, 0xff, sizeof(u64) * f->owner_words, s));
-        CUDA_TRY(cudaMemsetAsync(f->d_state, 0, sizeof(u32) * 4, s));
+        CUDA_TRY(cudaMemsetAsync(f->d_state, 0, sizeof(u32) * 8, s));
         f->rounds_bound = 0;
     }
     return BC_OK;
@@ -421,6 +440,13 @@ static int insert_device(bc_filter *f, u64 *words, const u64 *keys, u64 n, int m
     int rc = ensure_ordered_scratch(f, s);
     if (rc == BC_OK) rc = ordered_begin(f, s);
     if (rc) return rc;
+    if (ordered_ticket_supported(f->kp)) {
+        // small filters: a dataflow over per-block tickets (ordered_ticket.cu)
+        cudaError_t e = launch_ordered_ticket(f->kp, words, keys, n, s);
+        if (e != cudaSuccess) rc = fail(BC_ECUDA, "ordered ticket insert: %s", cudaGetErrorString(e));
+        const int rc2 = ordered_end(f, s);
+        return rc ? rc : rc2;
+    }
     for (u64 off = 0; off < n && rc == BC_OK; off += (1ull << 30)) {
         const u64 len = std::min<u64>(1ull << 30, n - off);
         rc = ordered_rearm(f, len, s);
@@ -574,6 +600,14 @@ extern "C" int bc_insert_qgrams(bc_filter *f, uint64_t *d_words, const uint8_t *
         int rc = ensure_ordered_scratch(f, s);
         if (rc == BC_OK) rc = ordered_begin(f, s);
         if (rc) return rc;
+        if (ordered_ticket_supported(f->kp)) {
+            cudaError_t e = launch_ordered_ticket_qgrams(f->kp, d_words, d_seq, nwin, q, canonical,
+                                                         slice_rec(record_len, 0), d_count, s);
+            if (e != cudaSuccess)
+                rc = fail(BC_ECUDA, "ordered ticket q-gram insert: %s", cudaGetErrorString(e));
+            const int rc2 = ordered_end(f, s);
+            return rc ? rc : rc2;
+        }
         for (u64 w = 0; w < nwin && rc == BC_OK; w += (1ull << 30)) {
             const u64 nw = std::min<u64>(1ull << 30, nwin - w);
             rc = ordered_rearm(f, nw, s);

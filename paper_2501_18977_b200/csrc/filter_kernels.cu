@@ -21,6 +21,7 @@
 #include <cooperative_groups.h>
 
 #include <atomic>
+#include <cstdio>
 #include <mutex>
 #include <unordered_map>
 
@@ -536,41 +537,73 @@ __global__ void __launch_bounds__(256) ordered_window_kernel(
 #ifndef BC_ORD_MINB
 #define BC_ORD_MINB 3  // <= 80 registers: 3 CTAs per SM (cfg3 +4%, cfg5 +8% over 2 CTAs at 102)
 #endif
+// Pending lists are CTA-local (shared memory): a key that loses a round is
+// retried by the CTA that holds it, so no grid-wide list or append counter
+// exists (one counter hammered by every warp's append was a serialised L2
+// hot spot, and the lists a DRAM round trip).  Each round every CTA refills
+// its list to `cap` entries with the next keys of the stream, taken with ONE
+// atomicAdd on a global cursor: the CTAs' slices of a round are disjoint and
+// together contiguous, and every slice of a round precedes every slice of
+// the next (a grid sync separates them), so keys still enter in index order
+// -- the invariant the commit rule needs.  Termination: in one round the sum
+// of the CTAs' pending counts (one atomic per CTA) is zero and some CTA's
+// slice reached the end of the stream (bit 31 of the same word: the cursor
+// itself cannot be compared after the sync, a fast CTA may already have
+// taken its next slice).
+// state (u32 x 8, zeroed before each launch): [0..2] rotating round words
+// (pending total | exhausted << 31), [4..5] the u64 stream cursor.
 template <int C, class Src>
 __global__ void __launch_bounds__(kTPB, BC_ORD_MINB) ordered512_kernel(
-    const __grid_constant__ KParams p, u64 *__restrict__ words, const Src src, u64 n, u64 window,
-    u32 *__restrict__ owner, u64 slots, u32 slot_shift, u32 *__restrict__ lists,
-    u64 *__restrict__ lkeys, u32 *__restrict__ state, unsigned long long *__restrict__ admitted) {
+    const __grid_constant__ KParams p, u64 *__restrict__ words, const Src src, u64 n, u32 cap,
+    u32 *__restrict__ owner, u64 slots, u32 slot_shift, u32 *__restrict__ state,
+    unsigned long long *__restrict__ admitted) {
     cg::grid_group grid = cg::this_grid();
     __shared__ WarpSmem<C> smem[kWarps];
+    __shared__ u32 s_cnt, s_pend, s_adm, s_exh;
+    __shared__ u64 s_start;
+    extern __shared__ __align__(16) unsigned char dsm[];
     WarpSmem<C> &ws = smem[threadIdx.x >> 5];
     const int lane = threadIdx.x & 31;
-    const u64 warp = blockIdx.x * (u64)kWarps + (threadIdx.x >> 5);
-    const u64 wstride = (u64)gridDim.x * kTPB;
-    u32 round = __ldcg(state);
-    // pending lists: the key's stream index (its priority) and the key itself,
-    // so a key that loses a round is neither re-read nor re-derived
-    u32 *cur = lists, *nxt = lists + window;
-    u64 *curk = lkeys, *nxtk = lkeys + window;
-    u64 npend = 0, next = 0;
+    const u32 wid = threadIdx.x >> 5;
+    // the CTA's pending lists: stream index (priority) and key, two buffers
+    u64 *curk = reinterpret_cast<u64 *>(dsm), *nxtk = curk + cap;
+    u32 *cur = reinterpret_cast<u32 *>(nxtk + cap), *nxt = cur + cap;
+    unsigned long long *cursor = reinterpret_cast<unsigned long long *>(state + 4);
+    if (threadIdx.x == 0) {
+        s_pend = 0;
+        s_cnt = 0;
+    }
+    u32 round = 0;
     u32 n_admitted = 0;
-    while (npend > 0 || next < n) {
-        const u64 admit = min(window - npend, n - next);
+#ifdef BC_ORD_PROF
+    long long t_work = 0, t_sync = 0, tq = clock64();
+    u32 ntiles = 0;
+#endif
+    for (;;) {
         u32 *own_cur = owner + (round & 1u) * slots;
         u32 *own_nxt = owner + ((round + 1u) & 1u) * slots;
-        u32 *cnt = state + 1 + round % 3u;
-        if (warp == 0 && lane == 0) state[1 + (round + 1u) % 3u] = 0;
-        const u64 total = npend + admit;
-        // tile entry t: a pending key from the list, or the next key of the
-        // stream (admit() is false for an index without a key)
-        auto fetch = [&](u64 t, u32 &li, u64 &x) -> bool {
+        if (threadIdx.x == 0) {
+            // refill to cap from the stream (s_pend: this CTA's losers of last round)
+            const u32 free = cap - s_pend;
+            const u64 st = free ? atomicAdd(cursor, (unsigned long long)free) : 0ull;
+            s_start = st;
+            s_adm = (free && st < n) ? (u32)min((u64)free, n - st) : 0u;
+            s_exh = free && st + free >= n;
+            s_cnt = 0;
+            if (blockIdx.x == 0) state[(round + 1u) % 3u] = 0;  // last read in round r-1
+        }
+        __syncthreads();
+        const u32 npend = s_pend, total = s_pend + s_adm;
+        const u64 start = s_start;
+        // tile entry t: a pending key from the list, or the next key of the slice
+        auto fetch = [&](u32 t, u32 &li, u64 &x) -> bool {
             if (t >= total) return false;
             if (t < npend) {
-                li = __ldcg(cur + t);
-                x = __ldcg(curk + t);
+                li = cur[t];
+                x = curk[t];
                 return true;
             }
-            const u64 idx = next + (t - npend);
+            const u64 idx = start + (t - npend);
             li = (u32)idx;
             const bool ok = src.admit(idx, x);
             n_admitted += ok ? 1u : 0u;
@@ -578,20 +611,19 @@ __global__ void __launch_bounds__(kTPB, BC_ORD_MINB) ordered512_kernel(
         };
         // warp-uniform tiles; the next tile's entries are fetched while the
         // current tile's candidate blocks are read and committed
-        u64 t0 = warp * 32;
+        u32 t0 = wid * 32;
         u32 li = 0;
         u64 x = 0;
         bool valid = fetch(t0 + lane, li, x);
         while (t0 < total) {
-            const u64 t = t0 + lane;
+            const u32 t = t0 + lane;
             const bool win = valid && t < npend && ordered_check(p, own_cur, slot_shift, x, li);
             const bool lose = valid && !win;
             if (lose) ordered_claim(p, own_nxt, slot_shift, x, li);
-            // reserve the losers' list slots now, store them after the commit
             const u32 lm = __ballot_sync(kFull, lose);
             u32 base = 0;
-            if (lm && lane == 0) base = atomicAdd(cnt, (u32)__popc(lm));
-            const u64 t1 = t0 + wstride;
+            if (lm && lane == 0) base = atomicAdd(&s_cnt, (u32)__popc(lm));
+            const u32 t1 = t0 + kTPB;
             u32 li_n = 0;
             u64 x_n = 0;
             const bool valid_n = fetch(t1 + lane, li_n, x_n);
@@ -613,10 +645,33 @@ __global__ void __launch_bounds__(kTPB, BC_ORD_MINB) ordered512_kernel(
             x = x_n;
             valid = valid_n;
             t0 = t1;
+#ifdef BC_ORD_PROF
+            ++ntiles;
+#endif
         }
+        __syncthreads();  // the round's local appends are complete
+        if (threadIdx.x == 0) {
+            s_pend = s_cnt;
+            if (s_cnt) atomicAdd(state + round % 3u, s_cnt);
+            if (s_exh) atomicOr(state + round % 3u, 0x80000000u);
+        }
+#ifdef BC_ORD_PROF
+        {
+            const long long t_ = clock64();
+            t_work += t_ - tq;
+            tq = t_;
+        }
+#endif
         grid.sync();
-        npend = __ldcg(cnt);
-        next += admit;
+#ifdef BC_ORD_PROF
+        {
+            const long long t_ = clock64();
+            t_sync += t_ - tq;
+            tq = t_;
+        }
+#endif
+        const u32 rw = __ldcg(state + round % 3u);
+        const bool more = (rw & 0x7fffffffu) != 0 || !(rw >> 31);
         u32 *tmp = cur;
         cur = nxt;
         nxt = tmp;
@@ -624,12 +679,17 @@ __global__ void __launch_bounds__(kTPB, BC_ORD_MINB) ordered512_kernel(
         curk = nxtk;
         nxtk = tmpk;
         ++round;
+        if (!more) break;
     }
     if (Src::kCounts && admitted != nullptr) {
         for (int o = 16; o > 0; o >>= 1) n_admitted += __shfl_xor_sync(kFull, n_admitted, o);
         if (lane == 0 && n_admitted) atomicAdd(admitted, (unsigned long long)n_admitted);
     }
-    if (warp == 0 && lane == 0) state[0] = round;
+#ifdef BC_ORD_PROF
+    if (lane == 0 && (blockIdx.x % 64) == 0 && wid == 0)
+        printf("ord prof cta %u rounds %u tiles %u work/round %lld sync/round %lld\n",
+               blockIdx.x, round, ntiles, t_work / max(round, 1u), t_sync / max(round, 1u));
+#endif
 }
 
 template <int OP>
@@ -1046,16 +1106,44 @@ static cudaError_t launch_window(const KParams &p, u64 *words, const Src *src, c
         attr[1].val.accessPolicyWindow.missProp = cudaAccessPropertyNormal;
         cfg.numAttrs = 2;
     }
-    count_launch();
     u32 *own = reinterpret_cast<u32 *>(owner);
-    if (!tile)
+    if (!tile) {
+        count_launch();
         return cudaLaunchKernelEx(&cfg, ordered_window_kernel, p, words, keys, n, chunk, own,
                                   slots, slot_shift, lists, state);
+    }
+    // CTA-local pending lists of `cap` entries (24 bytes each, two buffers):
+    // the window is spread over as many co-resident CTAs as fit, at least
+    // 256 entries per CTA
+    e = cudaMemsetAsync(state, 0, 8 * sizeof(u32), s);  // round words, cursor
+    if (e != cudaSuccess) return e;
+    const int sms = (int)sm_count();
+    u64 ctas = std::max<u64>(1, std::min<u64>((u64)sms * BC_ORD_MINB, chunk / 256));
+    u32 cap = 0;
+    size_t smem = 0;
+    for (int it = 0;; ++it) {
+        cap = (u32)((chunk + ctas - 1) / ctas);
+        smem = (size_t)cap * 24;
+        // static + dynamic shared memory above 48 KB needs the opt-in
+        if (cudaFuncSetAttribute(fw, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+            cudaSuccess)
+            return cudaErrorInvalidValue;
+        int per_sm = 0;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fw, 256, smem) != cudaSuccess ||
+            per_sm < 1)
+            return cudaErrorInvalidConfiguration;
+        if ((u64)per_sm * sms >= ctas) break;
+        if (it == 8) return cudaErrorInvalidConfiguration;
+        ctas = (u64)per_sm * sms;  // fewer co-resident CTAs: larger lists, re-check
+    }
+    cfg.gridDim = dim3((unsigned)ctas);
+    cfg.dynamicSmemBytes = smem;
+    count_launch();
     switch (p.c) {
 #define BC_ORD_C(c)                                                                         \
     case c:                                                                                 \
-        return cudaLaunchKernelEx(&cfg, ordered512_kernel<c, Src>, p, words, *src, n, chunk, \
-                                  own, slots, slot_shift, lists, lkeys, state, admitted);
+        return cudaLaunchKernelEx(&cfg, ordered512_kernel<c, Src>, p, words, *src, n, cap,   \
+                                  own, slots, slot_shift, state, admitted);
         BC_ORD_C(2) BC_ORD_C(3) BC_ORD_C(4) BC_ORD_C(5) BC_ORD_C(6) BC_ORD_C(7) BC_ORD_C(8)
 #undef BC_ORD_C
     }

@@ -24,6 +24,8 @@ struct ArrayKeys {
         x = __ldcs(keys + i);
         return true;
     }
+    // the same stream from key `off` on
+    __host__ __device__ void advance(u64 off) { keys += off; }
 };
 
 // 0x80 in every byte of b that is not one of A C G T a c g t.
@@ -59,6 +61,12 @@ struct SeqKeys {
     u64 qmask;      // low 2q bits
     u32 q;
     u32 canonical;
+
+    // the same stream from window `off` on
+    __host__ __device__ void advance(u64 off) {
+        seq += off;
+        if (rec.len) rec.phase = (rec.phase + off) % rec.len;
+    }
 
     // Window w's key: A=0 C=1 G=2 T=3 (either case), first base most
     // significant, canonical = min(code, reverse complement) -- the

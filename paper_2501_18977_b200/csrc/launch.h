@@ -80,6 +80,17 @@ cudaError_t launch_ordered_qgrams(const KParams &p, u64 *words, const u8 *seq, u
                                   u32 *lists, u64 *lkeys, u32 *state,
                                   unsigned long long *count, cudaStream_t s);
 
+// Exact stream-order insert of small filters as a dataflow (ordered_ticket.cu):
+// per-block tickets from a stable sort of (block, key) pairs, then keys commit
+// as soon as every earlier key sharing a block is done.  c in 2..8, 512-bit
+// blocks, random strategy, up to BC_TICKET_MAX_BLOCKS blocks (2^16).
+bool ordered_ticket_supported(const KParams &p);
+cudaError_t launch_ordered_ticket(const KParams &p, u64 *words, const u64 *keys, u64 n,
+                                  cudaStream_t s);
+cudaError_t launch_ordered_ticket_qgrams(const KParams &p, u64 *words, const u8 *seq, u64 nwin,
+                                         int q, int canonical, RecSpec rec,
+                                         unsigned long long *count, cudaStream_t s);
+
 // numpy PCG64 stream (default_rng(seed).integers(0, 2**64, uint64)) from a
 // seeded (state, inc): outputs [offset, offset+n), then & and_mask | or_mask.
 cudaError_t launch_pcg64_fill(u64 state_hi, u64 state_lo, u64 inc_hi, u64 inc_lo, u64 offset,

@@ -1,0 +1,304 @@
+// Exact stream-order insert (c >= 2, 512-bit blocks, random strategy) for
+// small filters, as a dataflow instead of claim rounds.
+//
+// The sequential rule (_kernels.py:133-174) makes key j depend on every
+// earlier key that shares a candidate block with it: those keys' writes must
+// be in the blocks j reads, and their reads must happen before j writes.
+// Every later key touching a block waits for every earlier one, so each
+// block is touched in stream order -- and nothing else is ordered.
+//
+//  1. tickets: for every (key, choice) pair, the number of earlier pairs on
+//     the same block, i.e. its rank in a stable sort of the pairs by block
+//     (cub::DeviceRadixSort over the block ids, then rank = sorted position -
+//     start of the block's run);
+//  2. execution: warps take 32-key tiles in stream order from a counter; a
+//     key is ready when every one of its blocks' done-counters equals its
+//     ticket there; it then reads its candidates, applies the reference's
+//     decision, writes the chosen block (nobody else may touch it until this
+//     key is done), and bumps the done-counter of every candidate
+//     (release).  Keys whose predecessor is still running poll their
+//     counters.
+//
+// No round barriers: the critical path is the longest chain of keys linked
+// by shared blocks (274 keys for config 1's 2^20 keys on 2^15 blocks), each
+// link one L2 round trip plus a commit, instead of one grid-wide round per
+// link.  Deadlock-free without residency assumptions: tiles are taken in
+// stream order and a warp takes its next tile only when it has finished the
+// current one, so the earliest unfinished key is always held by a running
+// warp and all its predecessors are done.
+#include <cub/device/device_radix_sort.cuh>
+
+#include <algorithm>
+#include <cstdlib>
+
+#include "blocks.cuh"
+#include "keysrc.cuh"
+#include "launch.h"
+
+#ifndef BC_TICKET_SLEEP
+#define BC_TICKET_SLEEP 32  // ns between polls of a warp with waiting keys (0: spin)
+#endif
+
+namespace bc {
+
+// Polls are relaxed (an acquire load would also invalidate L1 every time);
+// one acq_rel fence after the poll that sees a key ready, and one before a
+// key's counter increments, give the release/acquire pairing.
+__device__ __forceinline__ u32 ld_relaxed_u32(const u32 *p) {
+    u32 v;
+    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+__device__ __forceinline__ void fence_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
+
+__device__ __forceinline__ void red_relaxed_add(u32 *p, u32 v) {
+    asm volatile("red.relaxed.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// Pairs (block of choice ci of key j, pair id j*C + ci); keys that do not
+// exist (skipped q-gram windows) get the block id M, sorted past every real one.
+template <class Src>
+__global__ void __launch_bounds__(256) ticket_pairs_kernel(const __grid_constant__ KParams p,
+                                                           const Src src, u64 n, u32 *blk,
+                                                           u32 *pid) {
+    const u64 stride = (u64)gridDim.x * blockDim.x;
+    for (u64 j = blockIdx.x * (u64)blockDim.x + threadIdx.x; j < n; j += stride) {
+        u64 x;
+        const bool ok = src.admit(j, x);
+        for (u32 ci = 0; ci < p.c; ++ci) {
+            blk[j * p.c + ci] = ok ? (u32)block_index(p, x, ci) : (u32)p.num_blocks;
+            pid[j * p.c + ci] = (u32)(j * p.c + ci);
+        }
+    }
+}
+
+// start[b] = first sorted position of block b's run
+__global__ void __launch_bounds__(256) ticket_runs_kernel(const u32 *sblk, u64 m, u32 *start) {
+    const u64 stride = (u64)gridDim.x * blockDim.x;
+    for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < m; i += stride)
+        if (i == 0 || sblk[i - 1] != sblk[i]) start[sblk[i]] = (u32)i;
+}
+
+__global__ void __launch_bounds__(256) ticket_rank_kernel(const u32 *sblk, const u32 *spid, u64 m,
+                                                          const u32 *start, u32 *ticket) {
+    const u64 stride = (u64)gridDim.x * blockDim.x;
+    for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < m; i += stride)
+        ticket[spid[i]] = (u32)i - start[sblk[i]];
+}
+
+template <int C, class Src>
+__global__ void __launch_bounds__(256) ticket_exec_kernel(
+    const __grid_constant__ KParams p, u64 *__restrict__ words, const Src src, u64 n,
+    const u32 *__restrict__ ticket, u32 *__restrict__ done, u32 *__restrict__ tile_ctr,
+    unsigned long long *__restrict__ admitted) {
+    __shared__ u32 mcol[16][256];  // per-thread 512-bit mask columns
+    const u32 tid = threadIdx.x, lane = tid & 31;
+    u32 *col = &mcol[0][tid];
+    const u64 ntiles = (n + 31) / 32;
+    const uint4 *w4 = reinterpret_cast<const uint4 *>(words);
+    u32 n_adm = 0;
+    for (;;) {
+        u32 t = 0;
+        if (lane == 0) t = atomicAdd(tile_ctr, 1u);
+        t = __shfl_sync(kFull, t, 0);
+        if (t >= ntiles) break;
+        const u64 j = (u64)t * 32 + lane;
+        u64 x = 0;
+        const bool valid = j < n && src.admit(j, x);
+        n_adm += valid ? 1u : 0u;
+        u32 bl[C], want[C];
+        if (valid) {
+#pragma unroll
+            for (int ci = 0; ci < C; ++ci) {
+                bl[ci] = (u32)block_index(p, x, ci);
+                want[ci] = __ldg(ticket + j * C + ci);
+            }
+            // a block chosen twice by one key holds two consecutive tickets:
+            // the key is ready when the first of them is reached
+#pragma unroll
+            for (int ci = 1; ci < C; ++ci)
+#pragma unroll
+                for (int cj = 0; cj < ci; ++cj) want[ci] -= (u32)(bl[cj] == bl[ci]);
+#pragma unroll
+            for (int w = 0; w < 16; ++w) col[w * 256] = 0u;
+            const u32 xlo = (u32)x, xhi = (u32)(x >> 32);
+            for (u32 i = 0; i < p.k; ++i) {
+                const u32 hi = mul_hi32(p.bit_a_lo[i], p.bit_a_hi[i], xlo, xhi);
+                atomicOr(&col[(hi >> 28) * 256], 1u << ((hi >> 23) & 31u));
+            }
+        }
+        bool pend = valid;
+        while (__any_sync(kFull, pend)) {
+            if (pend) {
+                bool ready = true;
+#pragma unroll
+                for (int ci = 0; ci < C; ++ci) ready &= ld_relaxed_u32(done + bl[ci]) == want[ci];
+                if (ready) {
+                    fence_gpu();  // acquire: the predecessors' writes
+                    uint4 m[4], wv[C][4];
+#pragma unroll
+                    for (int ci = 0; ci < C; ++ci)
+#pragma unroll
+                        for (int q = 0; q < 4; ++q) wv[ci][q] = ld_block_cg(w4 + (u64)bl[ci] * 4 + q);
+#pragma unroll
+                    for (int q = 0; q < 4; ++q)
+                        m[q] = make_uint4(col[(4 * q) * 256], col[(4 * q + 1) * 256],
+                                          col[(4 * q + 2) * 256], col[(4 * q + 3) * 256]);
+                    bool noop = false;
+                    int best = 0;
+                    u32 best_r = 0xffffffffu;
+#pragma unroll
+                    for (int ci = 0; ci < C; ++ci) {
+                        u32 jj = 0, pres = 0;
+#pragma unroll
+                        for (int q = 0; q < 4; ++q) {
+                            const uint4 w = wv[ci][q];
+                            jj += popc4(make_uint4(w.x | m[q].x, w.y | m[q].y, w.z | m[q].z,
+                                                   w.w | m[q].w));
+                            pres += popc4(w);
+                        }
+                        noop |= jj == pres;
+                        const u32 r = __ldg(p.rank + jj * (p.k + 1) + (jj - pres));
+                        if (r < best_r) {
+                            best_r = r;
+                            best = ci;
+                        }
+                    }
+                    if (!noop) {
+#pragma unroll
+                        for (int ci = 0; ci < C; ++ci)
+                            if (ci == best)
+#pragma unroll
+                                for (int q = 0; q < 4; ++q) {
+                                    const uint4 w = wv[ci][q];
+                                    __stcg(reinterpret_cast<uint4 *>(words) + (u64)bl[ci] * 4 + q,
+                                           make_uint4(w.x | m[q].x, w.y | m[q].y, w.z | m[q].z,
+                                                      w.w | m[q].w));
+                                }
+                    }
+                    // release: the write is visible before any successor sees the
+                    // counters move
+                    fence_gpu();
+#pragma unroll
+                    for (int ci = 0; ci < C; ++ci) red_relaxed_add(done + bl[ci], 1u);
+                    pend = false;
+                }
+            }
+#if BC_TICKET_SLEEP
+            if (__any_sync(kFull, pend)) __nanosleep(BC_TICKET_SLEEP);
+#endif
+        }
+    }
+    if (Src::kCounts && admitted != nullptr) {
+        for (int o = 16; o > 0; o >>= 1) n_adm += __shfl_xor_sync(kFull, n_adm, o);
+        if (lane == 0 && n_adm) atomicAdd(admitted, (unsigned long long)n_adm);
+    }
+}
+
+// ---- host side -------------------------------------------------------------------------
+
+static u64 env_u64(const char *name, u64 dflt) {
+    const char *e = std::getenv(name);
+    return e ? std::strtoull(e, nullptr, 10) : dflt;
+}
+
+// Keys per ticket set (tickets are ranks within one set; sets run in stream
+// order; BC_TICKET_CHUNK overrides, for tests).
+static u64 ticket_chunk() { return std::max<u64>(1, env_u64("BC_TICKET_CHUNK", 1ull << 24)); }
+
+bool ordered_ticket_supported(const KParams &p) {
+    if (!(p.fast_random && p.wpb == 8 && p.c >= 2 && p.c <= 8)) return false;
+    if (env_u64("BC_ORDERED_TICKET", 1) == 0) return false;
+    return p.num_blocks <= env_u64("BC_TICKET_MAX_BLOCKS", 1ull << 16);
+}
+
+template <int C, class Src>
+static cudaError_t exec_launch(const KParams &p, u64 *words, const Src &src, u64 n,
+                               const u32 *ticket, u32 *done, u32 *ctr,
+                               unsigned long long *admitted, cudaStream_t s) {
+    // keys in flight (8 warps x 32 per CTA) ~ M (BC_TICKET_INFLIGHT_PCT of
+    // M): a window much wider than the filter only queues keys behind each
+    // other on the same blocks and floods L2 with polls
+    const void *fn = (const void *)ticket_exec_kernel<C, Src>;
+    const u64 inflight = std::max<u64>(256, p.num_blocks * env_u64("BC_TICKET_INFLIGHT_PCT", 100) / 100);
+    const unsigned grid = grid_for(fn, 256, 0, std::min<u64>((n + 255) / 256, (inflight + 255) / 256));
+    ticket_exec_kernel<C, Src><<<grid, 256, 0, s>>>(p, words, src, n, ticket, done, ctr, admitted);
+    count_launch();
+    return cudaGetLastError();
+}
+
+template <class Src>
+static cudaError_t ticket_insert(const KParams &p, u64 *words, const Src &src, u64 n,
+                                 unsigned long long *admitted, cudaStream_t s) {
+    if (n == 0) return cudaSuccess;
+    const u64 c = p.c, M = p.num_blocks;
+    const u64 per = std::min(n, ticket_chunk());
+    const u64 m = per * c;
+    int bits = 1;
+    while ((1ull << bits) <= M) ++bits;  // block ids 0..M (M marks a skipped window)
+    size_t cub_bytes = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, cub_bytes, (const u32 *)nullptr, (u32 *)nullptr,
+                                    (const u32 *)nullptr, (u32 *)nullptr, (int)m, 0, bits, s);
+    // scratch: blk in/out, pid in/out, ticket (m each), start + done (M + 1 each), counter
+    const size_t words32 = 5 * m + 2 * (M + 1) + 1;
+    const size_t cub_off = ((words32 * 4 + 255) / 256) * 256;
+    unsigned char *scratch = nullptr;
+    cudaError_t e = cudaMallocAsync((void **)&scratch, cub_off + cub_bytes, s);
+    if (e != cudaSuccess) return e;
+    u32 *blk = reinterpret_cast<u32 *>(scratch), *sblk = blk + m, *pid = sblk + m,
+        *spid = pid + m, *ticket = spid + m, *start = ticket + m, *done = start + (M + 1),
+        *ctr = done + (M + 1);
+    void *cub_tmp = scratch + cub_off;
+    const KParams &kp = p;
+    for (u64 off = 0; off < n && e == cudaSuccess; off += per) {
+        const u64 len = std::min(per, n - off);
+        const u64 ml = len * c;
+        Src sub = src;
+        sub.advance(off);
+        const unsigned g1 = grid_for((const void *)ticket_pairs_kernel<Src>, 256, 0,
+                                     (len + 255) / 256);
+        ticket_pairs_kernel<Src><<<g1, 256, 0, s>>>(kp, sub, len, blk, pid);
+        count_launch();
+        size_t tb = cub_bytes;
+        e = cub::DeviceRadixSort::SortPairs(cub_tmp, tb, blk, sblk, pid, spid, (int)ml, 0, bits,
+                                            s);
+        if (e != cudaSuccess) break;
+        const unsigned g2 = grid_for((const void *)ticket_runs_kernel, 256, 0, (ml + 255) / 256);
+        ticket_runs_kernel<<<g2, 256, 0, s>>>(sblk, ml, start);
+        ticket_rank_kernel<<<g2, 256, 0, s>>>(sblk, spid, ml, start, ticket);
+        count_launch(2);
+        e = cudaMemsetAsync(done, 0, sizeof(u32) * (M + 2), s);  // done[] and the tile counter
+        if (e != cudaSuccess) break;
+        switch (p.c) {
+#define BC_TK(cc) \
+    case cc: e = exec_launch<cc, Src>(kp, words, sub, len, ticket, done, ctr, admitted, s); break;
+            BC_TK(2) BC_TK(3) BC_TK(4) BC_TK(5) BC_TK(6) BC_TK(7) BC_TK(8)
+#undef BC_TK
+            default: e = cudaErrorInvalidValue;
+        }
+        if (e == cudaSuccess) e = cudaGetLastError();
+    }
+    cudaFreeAsync(scratch, s);
+    return e;
+}
+
+cudaError_t launch_ordered_ticket(const KParams &p, u64 *words, const u64 *keys, u64 n,
+                                  cudaStream_t s) {
+    const ArrayKeys src{keys};
+    return ticket_insert(p, words, src, n, nullptr, s);
+}
+
+cudaError_t launch_ordered_ticket_qgrams(const KParams &p, u64 *words, const u8 *seq, u64 nwin,
+                                         int q, int canonical, RecSpec rec,
+                                         unsigned long long *count, cudaStream_t s) {
+    SeqKeys src;
+    src.seq = seq;
+    src.rec = rec;
+    src.q = (u32)q;
+    src.canonical = (u32)canonical;
+    src.qmask = q == 32 ? ~0ull : ((1ull << (2 * q)) - 1ull);
+    return ticket_insert(p, words, src, nwin, count, s);
+}
+
+}  // namespace bc

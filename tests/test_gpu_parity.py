@@ -674,19 +674,33 @@ def test_ordered_build_with_hashed_claim_slots(golden, slots):
         f"keys = bb.even_keys({case['n_insert']}, {case['insert_seed']})\n"
         "f.insert_many(keys[:7000]); f.insert_many(keys[7000:])\n"
         "print(hashlib.sha256(f.storage.words.tobytes()).hexdigest())\n")
-    assert _run_with_env(script, BC_ORDERED_SLOTS=slots) == case["words_sha256"]
+    assert _run_with_env(script, BC_ORDERED_SLOTS=slots, BC_ORDERED_TICKET="0") == \
+        case["words_sha256"]
+
+
+GRID = {"BC_ORDERED_TICKET": "0"}  # exact inserts on the grid-wide claim rounds
 
 
 @pytest.mark.parametrize("name,env", [("cfg2_small", {"BC_LOOKUP_PIPE": "0"}),
-                                      ("bc3_k12_20k", {"BC_ORDERED_WINDOW": "0"}),
-                                      ("cfg1", {"BC_ORDERED_WINDOW": "0"}),
-                                      ("bc3_k12_20k", {"BC_ORDERED_TILES": "0"}),
-                                      ("cfg1", {"BC_ORDERED_TILES": "0"})])
+                                      ("bc3_k12_20k", {**GRID, "BC_ORDERED_WINDOW": "0"}),
+                                      ("cfg1", {**GRID, "BC_ORDERED_WINDOW": "0"}),
+                                      ("bc3_k12_20k", {**GRID, "BC_ORDERED_TILES": "0"}),
+                                      ("cfg1", {**GRID, "BC_ORDERED_TILES": "0"}),
+                                      ("cfg1", GRID), ("bc3_k12_20k", GRID),
+                                      ("bc4_k8", GRID), ("cfg3_small", GRID),
+                                      ("bc8_k5", GRID), ("bc2_k6_t4", GRID),
+                                      ("cfg1", {"BC_TICKET_INFLIGHT_PCT": "3"}),
+                                      ("cfg1", {"BC_TICKET_CHUNK": "100000"}),
+                                      ("bc3_k12_20k", {"BC_TICKET_CHUNK": "777",
+                                                       "BC_TICKET_INFLIGHT_PCT": "1000"}),
+                                      ("cfg5_small_k11", {"BC_TICKET_CHUNK": "65536"})])
 def test_fallback_kernels_match_reference(golden, name, env):
-    """The non-default kernel variants kept behind switches (unpipelined
-    single-choice lookups, fixed-chunk exact inserts, exact inserts that
-    commit one thread per key) still give the
-    reference's bits and answers."""
+    """The kernel variants kept behind switches (unpipelined single-choice
+    lookups, the grid-wide exact inserts that small filters no longer use,
+    fixed-chunk exact inserts, exact inserts that commit one thread per key)
+    and the ticket exact insert with narrow / wide in-flight windows and
+    several ticket sets per call still give the reference's bits and
+    answers."""
     meta, _ = golden
     case = meta[name]
     script = (
@@ -846,3 +860,27 @@ def test_concurrent_lookups_from_threads(golden):
     with ThreadPoolExecutor(8) as pool:
         counts = list(pool.map(g.count_hits, parts))
     assert sum(counts) == case["hits_pos"] + case["hits_neg"]
+
+
+@pytest.mark.parametrize("env", [{"BC_TICKET_CHUNK": "1000"}, {"BC_ORDERED_TICKET": "0"}])
+def test_fused_exact_qgram_insert_in_ticket_sets_and_claim_rounds(env):
+    """The fused exact-order q-gram insert of a reads matrix (fixed-length
+    records) split into many ticket sets (each set's stream resumes mid-record)
+    and on the grid-wide claim rounds equals the oracle's stream-order insert
+    of encode_qgrams."""
+    script = (
+        "import numpy as np, paper_2501_18977_b200 as bb\n"
+        "from oracle import oracle as orc\n"
+        "rng = np.random.default_rng(21)\n"
+        "reads = rng.choice(np.frombuffer(b'ACGTacgtN', np.uint8), size=(211, 97),\n"
+        "                   p=[0.124] * 8 + [0.008])\n"
+        "enc = bb.QGramEncoder(21, canonical=True)\n"
+        "want = np.concatenate([orc.encode_qgrams(r.tobytes(), 21, True) for r in reads])\n"
+        "f = bb.Filter.from_config(bb.FilterConfig(kind='blowchoc', k=9, choices=3,\n"
+        "                                          n_capacity=4000, seed=5))\n"
+        "assert f.insert_qgrams(enc, reads) == want.size\n"
+        "o = orc.make_filter('blowchoc', k=9, choices=3, n_capacity=4000, seed=5)\n"
+        "o.insert_many(want)\n"
+        "print(bool(np.array_equal(f.storage.words, o.words)), want.size)\n")
+    ok, n = _run_with_env(script, **env).split()
+    assert ok == "True" and int(n) > 10000
