@@ -534,9 +534,6 @@ __global__ void __launch_bounds__(256) ordered_window_kernel(
 #ifndef BC_ORD_UNR
 #define BC_ORD_UNR 0  // keys per load step of the commit (0: relaxed_unroll(C))
 #endif
-#ifndef BC_ORD_TWO_PHASE
-#define BC_ORD_TWO_PHASE 0  // ordered512_kernel: claims of a round first, then its commits
-#endif
 #ifndef BC_ORD_MINB
 #define BC_ORD_MINB 3  // <= 80 registers: 3 CTAs per SM (cfg3 +4%, cfg5 +8% over 2 CTAs at 102)
 #endif
@@ -568,16 +565,9 @@ __global__ void __launch_bounds__(kTPB, BC_ORD_MINB) ordered512_kernel(
     WarpSmem<C> &ws = smem[threadIdx.x >> 5];
     const int lane = threadIdx.x & 31;
     const u32 wid = threadIdx.x >> 5;
-    // the CTA's pending lists: stream index (priority) and key, two buffers;
-    // BC_ORD_TWO_PHASE: the round's winners' keys
+    // the CTA's pending lists: stream index (priority) and key, two buffers
     u64 *curk = reinterpret_cast<u64 *>(dsm), *nxtk = curk + cap;
-#if BC_ORD_TWO_PHASE
-    u64 *wink = nxtk + cap;
-    u32 *cur = reinterpret_cast<u32 *>(wink + cap), *nxt = cur + cap;
-    __shared__ u32 s_win;
-#else
     u32 *cur = reinterpret_cast<u32 *>(nxtk + cap), *nxt = cur + cap;
-#endif
     unsigned long long *cursor = reinterpret_cast<unsigned long long *>(state + 4);
     if (threadIdx.x == 0) {
         s_pend = 0;
@@ -600,9 +590,6 @@ __global__ void __launch_bounds__(kTPB, BC_ORD_MINB) ordered512_kernel(
             s_adm = (free && st < n) ? (u32)min((u64)free, n - st) : 0u;
             s_exh = free && st + free >= n;
             s_cnt = 0;
-#if BC_ORD_TWO_PHASE
-            s_win = 0;
-#endif
             if (blockIdx.x == 0) state[(round + 1u) % 3u] = 0;  // last read in round r-1
         }
         __syncthreads();
@@ -622,49 +609,6 @@ __global__ void __launch_bounds__(kTPB, BC_ORD_MINB) ordered512_kernel(
             n_admitted += ok ? 1u : 0u;
             return ok;
         };
-#if BC_ORD_TWO_PHASE
-        // phase A: claims only (L2): pending keys check theirs -- winners go
-        // to the CTA's winners list, losers claim again -- and new keys claim
-        for (u32 t0 = wid * 32; t0 < total; t0 += kTPB) {
-            u32 li = 0;
-            u64 x = 0;
-            const bool valid = fetch(t0 + lane, li, x);
-            const bool win =
-                valid && t0 + lane < npend && ordered_check(p, own_cur, slot_shift, x, li);
-            const bool lose = valid && !win;
-            if (lose) ordered_claim(p, own_nxt, slot_shift, x, li);
-            const u32 lm = __ballot_sync(kFull, lose), wm = __ballot_sync(kFull, win);
-            u32 lb = 0, wb = 0;
-            if (lane == 0) {
-                if (lm) lb = atomicAdd(&s_cnt, (u32)__popc(lm));
-                if (wm) wb = atomicAdd(&s_win, (u32)__popc(wm));
-            }
-            lb = __shfl_sync(kFull, lb, 0);
-            wb = __shfl_sync(kFull, wb, 0);
-            const u32 below = (1u << lane) - 1u;
-            if (lose) {
-                nxt[lb + __popc(lm & below)] = li;
-                nxtk[lb + __popc(lm & below)] = x;
-            }
-            if (win) wink[wb + __popc(wm & below)] = x;
-        }
-        __syncthreads();
-        // phase B: commit the winners (pairwise-disjoint blocks) in full tiles
-        {
-            const u32 nwin = s_win;
-            for (u32 t0 = wid * 32; t0 < nwin; t0 += kTPB) {
-                const bool valid = t0 + lane < nwin;
-                const u64 x = valid ? wink[t0 + lane] : 0ull;
-                phase1<C>(p, x, valid, ws, lane);
-                __syncwarp();
-                phase2<OP_INSERT, C, BC_ORD_UNR>(p, words, ws, lane);
-                __syncwarp();
-#ifdef BC_ORD_PROF
-                ++ntiles;
-#endif
-            }
-        }
-#else
         // warp-uniform tiles; the next tile's entries are fetched while the
         // current tile's candidate blocks are read and committed
         u32 t0 = wid * 32;
@@ -705,7 +649,6 @@ __global__ void __launch_bounds__(kTPB, BC_ORD_MINB) ordered512_kernel(
             ++ntiles;
 #endif
         }
-#endif
         __syncthreads();  // the round's local appends are complete
         if (threadIdx.x == 0) {
             s_pend = s_cnt;
@@ -1180,7 +1123,7 @@ static cudaError_t launch_window(const KParams &p, u64 *words, const Src *src, c
     size_t smem = 0;
     for (int it = 0;; ++it) {
         cap = (u32)((chunk + ctas - 1) / ctas);
-        smem = (size_t)cap * (BC_ORD_TWO_PHASE ? 32 : 24);
+        smem = (size_t)cap * 24;
         // static + dynamic shared memory above 48 KB needs the opt-in
         if (cudaFuncSetAttribute(fw, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
             cudaSuccess)
