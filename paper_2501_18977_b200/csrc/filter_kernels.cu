@@ -450,6 +450,27 @@ __device__ __forceinline__ bool ordered_check(const KParams &p, u32 *own_cur, u3
     return mine == (1u << p.c) - 1u;
 }
 
+// The same check with one atomicCAS(slot, li -> unclaimed) per distinct slot:
+// it reads the claim and resets it if it is this key's, in one L2 operation
+// instead of a load and a store.  A slot repeated among the key's candidates
+// is checked once (a second CAS would see it already reset).
+template <int C>
+__device__ __forceinline__ bool ordered_check_cas(const KParams &p, u32 *own_cur, u32 slot_shift,
+                                                  u64 x, u32 li) {
+    u64 sl[C];
+#pragma unroll
+    for (int ci = 0; ci < C; ++ci) sl[ci] = owner_slot(block_index(p, x, ci), slot_shift);
+    bool held = true;
+#pragma unroll
+    for (int ci = 0; ci < C; ++ci) {
+        bool dup = false;
+#pragma unroll
+        for (int cj = 0; cj < ci; ++cj) dup |= sl[cj] == sl[ci];
+        if (!dup) held &= atomicCAS(own_cur + sl[ci], li, kUnclaimed) == li;
+    }
+    return held;
+}
+
 __device__ __forceinline__ void ordered_claim(const KParams &p, u32 *own_nxt, u32 slot_shift,
                                               u64 x, u32 li) {
     for (u32 ci = 0; ci < p.c; ++ci)
@@ -534,6 +555,9 @@ __global__ void __launch_bounds__(256) ordered_window_kernel(
 #ifndef BC_ORD_UNR
 #define BC_ORD_UNR 0  // keys per load step of the commit (0: relaxed_unroll(C))
 #endif
+#ifndef BC_ORD_CAS
+#define BC_ORD_CAS 1  // claim checks as one atomicCAS per distinct slot
+#endif
 #ifndef BC_ORD_MINB
 #define BC_ORD_MINB 3  // <= 80 registers: 3 CTAs per SM (cfg3 +4%, cfg5 +8% over 2 CTAs at 102)
 #endif
@@ -577,7 +601,8 @@ __global__ void __launch_bounds__(kTPB, BC_ORD_MINB) ordered512_kernel(
     u32 n_admitted = 0;
 #ifdef BC_ORD_PROF
     long long t_work = 0, t_sync = 0, tq = clock64();
-    u32 ntiles = 0;
+    long long t_chk = 0, t_com = 0, t_rest = 0;
+    u32 ntiles = 0, ncom = 0;
 #endif
     for (;;) {
         u32 *own_cur = owner + (round & 1u) * slots;
@@ -616,23 +641,46 @@ __global__ void __launch_bounds__(kTPB, BC_ORD_MINB) ordered512_kernel(
         u64 x = 0;
         bool valid = fetch(t0 + lane, li, x);
         while (t0 < total) {
+#ifdef BC_ORD_PROF
+            const long long ta = clock64();
+#endif
             const u32 t = t0 + lane;
+#if BC_ORD_CAS
+            const bool win =
+                valid && t < npend && ordered_check_cas<C>(p, own_cur, slot_shift, x, li);
+#else
             const bool win = valid && t < npend && ordered_check(p, own_cur, slot_shift, x, li);
+#endif
             const bool lose = valid && !win;
             if (lose) ordered_claim(p, own_nxt, slot_shift, x, li);
             const u32 lm = __ballot_sync(kFull, lose);
+#ifdef BC_ORD_PROF
+            const long long tb_ = clock64();
+            t_chk += tb_ - ta;
+#endif
             u32 base = 0;
             if (lm && lane == 0) base = atomicAdd(&s_cnt, (u32)__popc(lm));
             const u32 t1 = t0 + kTPB;
             u32 li_n = 0;
             u64 x_n = 0;
             const bool valid_n = fetch(t1 + lane, li_n, x_n);
+#ifdef BC_ORD_PROF
+            const long long tc_ = clock64();
+            t_rest += tc_ - tb_;
+#endif
             if (__ballot_sync(kFull, win)) {  // tiles of admitted keys only claim
                 phase1<C>(p, x, win, ws, lane);
                 __syncwarp();
                 phase2<OP_INSERT, C, BC_ORD_UNR>(p, words, ws, lane);
                 __syncwarp();
+#ifdef BC_ORD_PROF
+                ++ncom;
+#endif
             }
+#ifdef BC_ORD_PROF
+            const long long td_ = clock64();
+            t_com += td_ - tc_;
+#endif
             if (lm) {
                 base = __shfl_sync(kFull, base, 0);
                 if (lose) {
@@ -687,8 +735,10 @@ __global__ void __launch_bounds__(kTPB, BC_ORD_MINB) ordered512_kernel(
     }
 #ifdef BC_ORD_PROF
     if (lane == 0 && (blockIdx.x % 64) == 0 && wid == 0)
-        printf("ord prof cta %u rounds %u tiles %u work/round %lld sync/round %lld\n",
-               blockIdx.x, round, ntiles, t_work / max(round, 1u), t_sync / max(round, 1u));
+        printf("ord prof cta %u rounds %u tiles %u (commit %u) work/round %lld sync/round %lld "
+               "per tile: check %lld fetch %lld commit-tile %lld\n",
+               blockIdx.x, round, ntiles, ncom, t_work / max(round, 1u), t_sync / max(round, 1u),
+               t_chk / max(ntiles, 1u), t_rest / max(ntiles, 1u), t_com / max(ncom, 1u));
 #endif
 }
 
