@@ -555,6 +555,9 @@ __global__ void __launch_bounds__(256) ordered_window_kernel(
 #ifndef BC_ORD_UNR
 #define BC_ORD_UNR 0  // keys per load step of the commit (0: relaxed_unroll(C))
 #endif
+#ifndef BC_ORD_DYN
+#define BC_ORD_DYN 1  // claim rounds: tiles after each warp's first taken from a CTA counter
+#endif
 #ifndef BC_ORD_CAS
 #define BC_ORD_CAS 1  // claim checks as one atomicCAS per distinct slot
 #endif
@@ -583,7 +586,7 @@ __global__ void __launch_bounds__(kTPB, BC_ORD_MINB) ordered512_kernel(
     unsigned long long *__restrict__ admitted) {
     cg::grid_group grid = cg::this_grid();
     __shared__ WarpSmem<C> smem[kWarps];
-    __shared__ u32 s_cnt, s_pend, s_adm, s_exh;
+    __shared__ u32 s_cnt, s_pend, s_adm, s_exh, s_tile;
     __shared__ u64 s_start;
     extern __shared__ __align__(16) unsigned char dsm[];
     WarpSmem<C> &ws = smem[threadIdx.x >> 5];
@@ -615,6 +618,7 @@ __global__ void __launch_bounds__(kTPB, BC_ORD_MINB) ordered512_kernel(
             s_adm = (free && st < n) ? (u32)min((u64)free, n - st) : 0u;
             s_exh = free && st + free >= n;
             s_cnt = 0;
+            s_tile = kTPB;  // tiles past the first one per warp, handed out on demand
             if (blockIdx.x == 0) state[(round + 1u) % 3u] = 0;  // last read in round r-1
         }
         __syncthreads();
@@ -637,6 +641,15 @@ __global__ void __launch_bounds__(kTPB, BC_ORD_MINB) ordered512_kernel(
         // warp-uniform tiles; the next tile's entries are fetched while the
         // current tile's candidate blocks are read and committed
         u32 t0 = wid * 32;
+#if BC_ORD_DYN
+        // the warps' first tiles are static; later ones go to whichever warp
+        // is free first, so a slow tile does not hold up its warp's share
+        auto next_tile = [&]() -> u32 {
+            u32 v = 0;
+            if (lane == 0) v = atomicAdd(&s_tile, 32u);
+            return __shfl_sync(kFull, v, 0);
+        };
+#endif
         u32 li = 0;
         u64 x = 0;
         bool valid = fetch(t0 + lane, li, x);
@@ -660,7 +673,11 @@ __global__ void __launch_bounds__(kTPB, BC_ORD_MINB) ordered512_kernel(
 #endif
             u32 base = 0;
             if (lm && lane == 0) base = atomicAdd(&s_cnt, (u32)__popc(lm));
+#if BC_ORD_DYN
+            const u32 t1 = next_tile();
+#else
             const u32 t1 = t0 + kTPB;
+#endif
             u32 li_n = 0;
             u64 x_n = 0;
             const bool valid_n = fetch(t1 + lane, li_n, x_n);
