@@ -570,10 +570,17 @@ def run_ours(args, cfg):
     words = filt.storage.d_words
     stream = torch.cuda.current_stream()
     # N > 1: order-free kinds (c = 1, standard) build from per-rank key slices
-    # and OR-all-reduce the replicas; c >= 2 builds on rank 0 and broadcasts
+    # and OR-all-reduce the replicas; relaxed c >= 2 builds are partitioned
+    # over the ranks' replicas through peer memory (one kernel per rank,
+    # distributed.build_partitioned) when the GPUs reach each other, else
+    # rank 0 builds and broadcasts
     split = DIST and world > 1 and D.order_free(filt)
-    builder = split or rank == 0
-    lo, hi = D.slice_bounds(cfg["n"], world)[rank] if split else (0, cfg["n"])
+    reps = None
+    if DIST and world > 1 and not split and mode == "relaxed" and D.partitionable(filt):
+        reps = D.peer_map(filt)  # collective; None on every rank if any cannot map
+    parted = reps is not None
+    builder = split or parted or rank == 0
+    lo, hi = D.slice_bounds(cfg["n"], world)[rank] if (split or parted) else (0, cfg["n"])
     my_keys = keys[lo:hi]
 
     def lookups():
@@ -583,13 +590,16 @@ def run_ours(args, cfg):
 
     def step(ev):
         ev[0].record(stream)
-        if builder:
+        if parted:
+            words.zero_()
+            D.build_partitioned(filt, keys, reps=reps)  # inserts, then the owners' broadcasts
+        elif builder:
             words.zero_()
             filt.insert_many(my_keys)
         ev[1].record(stream)
         if split:
             D.or_allreduce_(words.view(torch.int64))
-        elif DIST:
+        elif DIST and not parted:
             dist.broadcast(words.view(torch.int64), src=0)
         ev[2].record(stream)
         lookups()
@@ -670,6 +680,9 @@ def run_ours(args, cfg):
                    "parallelism": ("single GPU" if world == 1 else
                                    f"build from per-rank key slices + OR all-reduce, "
                                    f"lookups split dp{world}" if split else
+                                   f"relaxed build partitioned over the {world} replicas "
+                                   f"through peer memory (one kernel per rank) + the owners' "
+                                   f"range broadcasts, lookups split dp{world}" if parted else
                                    f"build on rank 0 + NCCL broadcast, lookups split dp{world}"),
                    "l2": "inputs larger than L2 (keys and queries re-read every step); filter "
                          "words L2-persisting only when the filter fits L2"},
@@ -677,7 +690,8 @@ def run_ours(args, cfg):
         "lookup_mkeys_s": round(world * plan["per_rank"] / look_ms / 1e3, 2),
         "lookup_ms": round(look_ms, 3), "insert_ms": round(ins_ms, 3) if builder else None,
         "broadcast_ms": round(bc_ms, 3) if DIST else None,
-        "replication": ("or_allreduce" if split else "broadcast") if DIST else None,
+        "replication": ("or_allreduce" if split else "partitioned" if parted else "broadcast")
+        if DIST else None,
         "false_negatives": fn, "fpr": fp / max(n_neg, 1), "negatives_checked": n_neg,
         "gpu_launches": int(launches),
         "clocks": clocks,
@@ -699,7 +713,7 @@ def run_ours(args, cfg):
         line["ordered_insert_mkeys_s"] = round(cfg["n"] / e0.elapsed_time(e1) / 1e3, 2)
         del exact
         torch.cuda.empty_cache()
-    if not args.no_extras and args.config == 5 and builder:
+    if not args.no_extras and args.config == 5 and rank == 0:
         line["fpr_curve"] = fpr_curve(filt, keys, dev)
     # e2e through the public API from page-locked host buffers
     if not args.no_e2e:

@@ -211,6 +211,22 @@ BC_API int bc_peer_span(uint64_t nwords, int world, uint64_t *span);
 BC_API int bc_or_allreduce_peers(uint64_t *const *h_peer_words, int world, int rank,
                                  uint64_t nwords, void *stream);
 
+/* Relaxed insert of this rank's key slice into a filter PARTITIONED over the
+ * ranks' replicas (the multi-GPU build of multi-choice filters,
+ * distributed.py): rank r's replica holds the authoritative words of blocks
+ * [r*per, (r+1)*per), per = ceil(M / nparts); h_parts is a host array of the
+ * replicas' addresses on this device (own one included; peers mapped with
+ * bc_ipc_import).  Each key reads its candidates and ORs its mask into the
+ * chosen block in the owner's replica, over NVLink when remote -- one kernel,
+ * no separate exchange.  keys_in_flight bounds this rank's keys in flight
+ * (0: M/2); the caller passes its share of M/2 so the whole build keeps the
+ * relaxed tolerance.  All ranks' calls run between two cross-rank barriers;
+ * an all-gather of the ranges then replicates the filter.  c in 2..4,
+ * 512-bit blocks, random strategy (BC_EUNSUP otherwise). */
+BC_API int bc_insert_peers(bc_filter *f, uint64_t *const *h_parts, int nparts,
+                           const uint64_t *d_keys, uint64_t n, uint64_t keys_in_flight,
+                           void *stream);
+
 /* Thread-local description of the last error on this thread. */
 BC_API const char *bc_last_error(void);
 

@@ -27,7 +27,7 @@ EXPORTS = (
     "bc_contains_qgrams", "bc_block_histogram", "bc_route", "bc_eval_hash",
     "bc_last_error", "bc_launch_count", "bc_version", "bc_pcg64_fill", "bc_l2_release",
     "bc_format_answers", "bc_parse_keys_text", "bc_ipc_export", "bc_ipc_import",
-    "bc_ipc_close", "bc_peer_span", "bc_or_allreduce_peers",
+    "bc_ipc_close", "bc_peer_span", "bc_or_allreduce_peers", "bc_insert_peers",
 )
 
 
@@ -100,6 +100,7 @@ def lib() -> ctypes.CDLL:
         L.bc_ipc_close.argtypes = [P, u64]
         L.bc_peer_span.argtypes = [u64, ci, P]
         L.bc_or_allreduce_peers.argtypes = [P, ci, ci, u64, P]
+        L.bc_insert_peers.argtypes = [P, P, ci, P, u64, u64, P]
         for name in EXPORTS:
             fn = getattr(L, name)
             if fn.restype is ctypes.c_int or name in (
@@ -108,7 +109,7 @@ def lib() -> ctypes.CDLL:
                     "bc_contains_qgrams", "bc_block_histogram", "bc_route", "bc_eval_hash",
                     "bc_pcg64_fill", "bc_format_answers", "bc_parse_keys_text",
                     "bc_ipc_export", "bc_ipc_import", "bc_ipc_close", "bc_peer_span",
-                    "bc_or_allreduce_peers"):
+                    "bc_or_allreduce_peers", "bc_insert_peers"):
                 fn.restype = ctypes.c_int
         _lib = L
         atexit.register(L.bc_l2_release)

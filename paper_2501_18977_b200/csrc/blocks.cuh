@@ -134,19 +134,41 @@ __device__ __forceinline__ uint4 sel4(const uint4 (&M)[4], int i) {
 // (the next tile's phase 1) with the loads.
 constexpr int relaxed_unroll(int C) { return C <= 2 ? 4 : (C <= 4 ? 2 : 1); }
 
-template <int C, int UNR>
-__device__ __forceinline__ void relaxed_load(const WarpSmem<C> &ws, const uint4 *w4, int lane,
-                                             int p0, uint4 (&w)[UNR][C]) {
+// Where block b's eight words are.  LocalWords: one array.  PartWords: the
+// filter spread over the replicas of a partitioned multi-GPU build (block b
+// is read and written in the replica of rank b / per, mapped into this
+// process over peer memory, at the same offset).
+struct LocalWords {
+    u64 *words;
+    __device__ __forceinline__ u64 *block(u64 b) const { return words + b * 8; }
+};
+
+struct PartWords {
+    u64 *part[kMaxParts];  // rank r's replica (this process's address of it)
+    u64 per;               // blocks per rank (ranks own contiguous block ranges)
+    u64 magic;             // floor(2^64 / per)
+    __device__ __forceinline__ u64 *block(u64 b) const {
+        u64 q = __umul64hi(b, magic);
+        if (b - q * per >= per) ++q;  // the estimate is exact or one short (common.cuh)
+        return part[q] + b * 8;
+    }
+};
+
+template <int C, int UNR, class A = LocalWords>
+__device__ __forceinline__ void relaxed_load(const WarpSmem<C> &ws, const A &a, int lane, int p0,
+                                             uint4 (&w)[UNR][C]) {
     const int g = lane >> 2, s = lane & 3;
 #pragma unroll
     for (int u = 0; u < UNR; ++u)
 #pragma unroll
         for (int ci = 0; ci < C; ++ci)
-            w[u][ci] = ld_block_cg(w4 + (u64)ws.blk[ci][4 * g + p0 + u] * 4 + s);
+            w[u][ci] = ld_block_cg(reinterpret_cast<const uint4 *>(
+                                       a.block(ws.blk[ci][4 * g + p0 + u])) +
+                                   s);
 }
 
-template <int C, int UNR>
-__device__ __forceinline__ void relaxed_commit(const KParams &p, u64 *words,
+template <int C, int UNR, class A = LocalWords>
+__device__ __forceinline__ void relaxed_commit(const KParams &p, const A &a,
                                                const WarpSmem<C> &ws, const uint4 (&M)[4],
                                                int lane, int p0, const uint4 (&w)[UNR][C]) {
     const int g = lane >> 2, s = lane & 3;
@@ -194,7 +216,7 @@ __device__ __forceinline__ void relaxed_commit(const KParams &p, u64 *words,
         }
         if (!noop) {
             const uint4 m = sel4(M, (p0 + u - s) & 3);
-            u64 *dst = words + (u64)ws.blk[best][4 * g + p0 + u] * 8 + 2 * s;
+            u64 *dst = a.block(ws.blk[best][4 * g + p0 + u]) + 2 * s;
             red_or_all(dst, (u64)m.x | ((u64)m.y << 32));
             red_or_all(dst + 1, (u64)m.z | ((u64)m.w << 32));
         }
@@ -238,8 +260,9 @@ __device__ __forceinline__ u32 phase2(const KParams &p, u64 *words, WarpSmem<C> 
 #pragma unroll
         for (int p0 = 0; p0 < 4; p0 += UNR) {
             uint4 w[UNR][C];
-            relaxed_load<C, UNR>(ws, w4, lane, p0, w);
-            relaxed_commit<C, UNR>(p, words, ws, M, lane, p0, w);
+            const LocalWords lw{words};
+            relaxed_load<C, UNR>(ws, lw, lane, p0, w);
+            relaxed_commit<C, UNR>(p, lw, ws, M, lane, p0, w);
         }
         return 0;
     } else {

@@ -1070,6 +1070,33 @@ static int host_pipeline(bc_filter *f, u64 *words, const u64 *h_keys, u64 n, int
     return rc;
 }
 
+extern "C" int bc_insert_peers(bc_filter *f, uint64_t *const *h_parts, int nparts,
+                               const uint64_t *d_keys, uint64_t n, uint64_t keys_in_flight,
+                               void *stream) {
+    if (!f) return fail(BC_EINVAL, "null filter");
+    if (!h_parts || nparts < 1 || nparts > kMaxParts)
+        return fail(BC_EINVAL, "nparts must be in [1, %d]", kMaxParts);
+    if (n && !d_keys) return fail(BC_EINVAL, "null keys");
+    for (int r = 0; r < nparts; ++r) {
+        if (!h_parts[r]) return fail(BC_EINVAL, "null replica pointer %d", r);
+        if (reinterpret_cast<uintptr_t>(h_parts[r]) % 64)
+            return fail(BC_EINVAL, "replica %d is not 64-byte aligned", r);
+    }
+    if (f->kind == BC_KIND_STANDARD || f->kp.c < 2 || f->kp.c > 4 || !f->kp.fast_random ||
+        f->kp.wpb != 8)
+        return fail(BC_EUNSUP,
+                    "partitioned inserts need 2..4 choices, 512-bit blocks, random strategy");
+    if (int rc = check_device(f)) return rc;
+    if (n == 0) return BC_OK;
+    KParams kp = f->kp;
+    // keys in flight: 256 per CTA (relaxed512 tiles); the caller's share of
+    // the M/2 the relaxed tolerance is stated for
+    const u64 inflight = keys_in_flight ? keys_in_flight : std::max<u64>(1, kp.num_blocks / 2);
+    kp.max_ctas = (u32)std::max<u64>(1, std::min<u64>(inflight / 256, 0xffffffffu));
+    CUDA_TRY(launch_relaxed_peers(kp, h_parts, nparts, d_keys, n, (cudaStream_t)stream));
+    return BC_OK;
+}
+
 extern "C" int bc_insert_host(bc_filter *f, uint64_t *d_words, const uint64_t *h_keys,
                               uint64_t n, int mode, void *stream) {
     if (!f) return fail(BC_EINVAL, "null filter");

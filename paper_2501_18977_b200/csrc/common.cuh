@@ -30,6 +30,7 @@ struct DevHash {
 constexpr int kMaxChoices = 8;
 constexpr int kMaxFastK = 64;   // bit multipliers passed by value up to this k
 constexpr int kMaxWpb = 64;     // generic path: block_bits <= 4096
+constexpr int kMaxParts = 16;   // ranks of a partitioned (multi-GPU) build
 
 // Everything a kernel needs about one filter, passed by value (param space).
 struct KParams {

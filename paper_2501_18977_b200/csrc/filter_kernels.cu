@@ -108,15 +108,13 @@ __global__ void __launch_bounds__(kTPB) blocks512_kernel(const __grid_constant__
 // next tile's phase 1 (hashing, mask build -- no filter reads, so those keys
 // are not yet in flight) issued while the current tile's candidate loads are
 // outstanding.  Double-buffered warp slices.
-template <int C>
-__global__ void __launch_bounds__(kTPB) relaxed512_kernel(const __grid_constant__ KParams p,
-                                                          u64 *__restrict__ words,
-                                                          const u64 *__restrict__ keys, u64 n) {
+template <int C, class A>
+__device__ __forceinline__ void relaxed512_loop(const KParams &p, const A &a,
+                                                const u64 *__restrict__ keys, u64 n) {
     constexpr int UNR = relaxed_unroll(C);
     __shared__ WarpSmem<C> smem[kWarps][2];
     WarpSmem<C> *ws = smem[threadIdx.x >> 5];
     const int lane = threadIdx.x & 31;
-    const uint4 *w4 = reinterpret_cast<const uint4 *>(words);
     const u64 ntiles = (n + 31) / 32;
     const u64 nwarps = (u64)gridDim.x * kWarps;
     u64 tile = blockIdx.x * (u64)kWarps + (threadIdx.x >> 5);
@@ -132,21 +130,39 @@ __global__ void __launch_bounds__(kTPB) relaxed512_kernel(const __grid_constant_
         uint4 M[4];
         read_masks<C>(cur, lane, false, M);
         uint4 w[UNR][C];
-        relaxed_load<C, UNR>(cur, w4, lane, 0, w);
+        relaxed_load<C, UNR>(cur, a, lane, 0, w);
         // the next tile's phase 1 while the loads are in flight
         const u64 nt = tile + nwarps;
         const bool vn = nt * 32 + lane < n;
         phase1<C>(p, x_next, vn, ws[b ^ 1], lane);
         i = (nt + nwarps) * 32 + lane;
         x_next = i < n ? ld_stream(keys + i) : 0ull;
-        relaxed_commit<C, UNR>(p, words, cur, M, lane, 0, w);
+        relaxed_commit<C, UNR>(p, a, cur, M, lane, 0, w);
 #pragma unroll
         for (int p0 = UNR; p0 < 4; p0 += UNR) {
-            relaxed_load<C, UNR>(cur, w4, lane, p0, w);
-            relaxed_commit<C, UNR>(p, words, cur, M, lane, p0, w);
+            relaxed_load<C, UNR>(cur, a, lane, p0, w);
+            relaxed_commit<C, UNR>(p, a, cur, M, lane, p0, w);
         }
         b ^= 1;
     }
+}
+
+template <int C>
+__global__ void __launch_bounds__(kTPB) relaxed512_kernel(const __grid_constant__ KParams p,
+                                                          u64 *__restrict__ words,
+                                                          const u64 *__restrict__ keys, u64 n) {
+    relaxed512_loop<C>(p, LocalWords{words}, keys, n);
+}
+
+// The same relaxed insert into a filter partitioned over the ranks' replicas
+// (multi-GPU build over peer memory, bc_insert_peers): block reads and REDs
+// go to the replica of the block's owner rank, over NVLink when remote.
+template <int C>
+__global__ void __launch_bounds__(kTPB) relaxed512_peer_kernel(const __grid_constant__ KParams p,
+                                                               const __grid_constant__ PartWords pw,
+                                                               const u64 *__restrict__ keys,
+                                                               u64 n) {
+    relaxed512_loop<C>(p, pw, keys, n);
 }
 
 // Lookups, 512-bit blocks, random strategy: staged blocks + per-address test
@@ -1057,6 +1073,29 @@ static cudaError_t launch512(const KParams &p, u64 *words, const u64 *keys, u64 
     unsigned grid = grid_for(fn, kTPB, 0, (n + kTPB - 1) / kTPB);
     if (p.max_ctas && grid > p.max_ctas) grid = p.max_ctas;
     return launch_words(blocks512_kernel<OP, C>, grid, p, words, s, p, words, keys, n, out, hits);
+}
+
+cudaError_t launch_relaxed_peers(const KParams &p, u64 *const *parts, int nparts,
+                                 const u64 *keys, u64 n, cudaStream_t s) {
+    if (n == 0) return cudaSuccess;
+    if (nparts < 1 || nparts > kMaxParts || !p.fast_random || p.wpb != 8 || p.c < 2 || p.c > 4)
+        return cudaErrorInvalidValue;
+    PartWords pw{};
+    for (int r = 0; r < nparts; ++r) pw.part[r] = parts[r];
+    pw.per = (p.num_blocks + nparts - 1) / nparts;
+    pw.magic = ~0ull / pw.per;  // floor((2^64 - 1) / per): still exact or one short
+    const void *fn = p.c == 2 ? (const void *)relaxed512_peer_kernel<2>
+                   : p.c == 3 ? (const void *)relaxed512_peer_kernel<3>
+                              : (const void *)relaxed512_peer_kernel<4>;
+    unsigned grid = grid_for(fn, kTPB, 0, (n + kTPB - 1) / kTPB);
+    if (p.max_ctas && grid > p.max_ctas) grid = p.max_ctas;
+    count_launch();
+    switch (p.c) {
+        case 2: relaxed512_peer_kernel<2><<<grid, kTPB, 0, s>>>(p, pw, keys, n); break;
+        case 3: relaxed512_peer_kernel<3><<<grid, kTPB, 0, s>>>(p, pw, keys, n); break;
+        default: relaxed512_peer_kernel<4><<<grid, kTPB, 0, s>>>(p, pw, keys, n); break;
+    }
+    return cudaGetLastError();
 }
 
 template <int OP>

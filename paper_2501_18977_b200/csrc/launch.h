@@ -27,6 +27,14 @@ unsigned grid_for(const void *kernel, int threads, size_t dyn_smem, unsigned lon
 cudaError_t launch_blocks(int op, const KParams &p, u64 *words, const u64 *keys, u64 n,
                           u8 *out, unsigned long long *hits, cudaStream_t s);
 
+// Relaxed insert (c in 2..4, 512-bit blocks, random strategy) into a filter
+// partitioned over nparts replicas: rank r's replica holds the authoritative
+// words of blocks [r*per, (r+1)*per), per = ceil(M / nparts); parts[r] is this
+// process's address of rank r's replica (peer memory).  p.max_ctas bounds the
+// keys in flight (256 per CTA).
+cudaError_t launch_relaxed_peers(const KParams &p, u64 *const *parts, int nparts,
+                                 const u64 *keys, u64 n, cudaStream_t s);
+
 // Exact stream-order insert for c >= 2 (claim rounds, one cooperative launch).
 // owner: the claim arrays, ordered_owner_words(num_blocks, slots) u64 words,
 // all-ones before the first launch (slots == num_blocks: one per block, else

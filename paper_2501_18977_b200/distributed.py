@@ -399,6 +399,77 @@ def build_subfilters(filt, keys, group=None, mode: str | None = None):
     return filt
 
 
+# -- partitioned multi-choice build over peer memory ----------------------------------
+
+def partitionable(filt) -> bool:
+    """Filters the partitioned relaxed build covers (bc_insert_peers): one
+    shard, 2..4 choices, 512-bit blocks, random bit strategy."""
+    return (filt.kind == "blowchoc" and 2 <= filt.choices <= 4 and filt.block_bits == 512
+            and filt.strategy == "random" and filt.shards == 1)
+
+
+def part_ranges(num_blocks: int, world: int) -> list:
+    """Word ranges [lo, hi) of the ranks' partitions: rank r owns blocks
+    [r*per, (r+1)*per), per = ceil(M / W) (the kernel's split)."""
+    per = -(-num_blocks // world)
+    return [(min(num_blocks, r * per) * 8, min(num_blocks, (r + 1) * per) * 8)
+            for r in range(world)]
+
+
+def peer_map(filt, group=None):
+    """The ranks' replicas of ``filt`` mapped into this process (collective;
+    None on every rank when any rank cannot map them)."""
+    return _peer_replicas(_words_i64(filt), group)
+
+
+def build_partitioned(filt, keys, group=None, reps=None) -> bool:
+    """Relaxed multi-choice build spread over the GPUs, for T = 1 filters
+    the reference builds on one writer (c >= 2).
+
+    Every rank inserts its contiguous slice of the stream (``keys`` is the
+    whole stream, identical on every rank) into ONE filter partitioned over
+    the ranks' replicas: block b lives in the replica of rank b / per, and
+    each key's candidate reads and its RED go there, over NVLink when remote
+    (one ``bc_insert_peers`` kernel per rank, between two cross-rank
+    barriers).  The ranks' keys in flight add up to M/2, the bound the relaxed
+    tolerance is stated for, so the result is a relaxed build like the
+    single-GPU one.  The owners' ranges are then broadcast so every rank
+    holds the whole filter.  Replaces rank-0 build + broadcast, which leaves
+    W - 1 GPUs idle during the build.
+
+    Returns False, having done nothing, when the replicas cannot be mapped
+    (the decision is collective), so the caller can fall back to
+    ``build_subfilters``."""
+    from . import _native
+
+    rank, world = _rank_world(group)
+    if not partitionable(filt):
+        raise ValueError("partitioned builds need T = 1, 2..4 choices, 512-bit random blocks")
+    words = _words_i64(filt)
+    if reps is None:
+        reps = peer_map(filt, group)
+    if reps is None:
+        return False
+    dev = words.device
+    part, lo, hi = _local_slice(keys, group)
+    if not isinstance(part, torch.Tensor):
+        part = torch.from_numpy(np.ascontiguousarray(part, dtype=np.uint64).view(np.int64))
+    part = part.to(dev).contiguous()
+    share = max(256, (filt.num_blocks // 2) // world)
+    _device_barrier(group, dev)  # every replica holds the filter before any remote write
+    stream = torch.cuda.current_stream(dev).cuda_stream
+    _native.check(_native.lib().bc_insert_peers(
+        ctypes.c_void_p(filt.handle), reps.ptrs, world, ctypes.c_void_p(part.data_ptr()),
+        part.numel(), share, ctypes.c_void_p(stream)))
+    _device_barrier(group, dev)  # every rank's inserts are in
+    for r, (a, b) in enumerate(part_ranges(filt.num_blocks, world)):
+        if b > a:
+            dist.broadcast(words[a:b], src=r, group=group)
+    filt.inserted += len(keys)
+    filt.storage.device_modified()
+    return True
+
+
 def exchange_by_shard(filt, local_keys, group=None):
     """Route a rank-local slice of the stream to the shard owners
     (all-to-all).  Rank r is assumed to hold the r-th contiguous part of the

@@ -265,3 +265,127 @@ def test_peer_or_allreduce_two_processes_one_gpu():
     merge kernel, and both hold the sequential build.  No kernel waits on the
     other rank (the barriers are on the host)."""
     mp.spawn(_peer_worker, args=(2, free_port()), nprocs=2, join=True)
+
+
+# -- partitioned multi-choice build (bc_insert_peers) ------------------------------------
+
+def test_part_ranges_cover():
+    from paper_2501_18977_b200.distributed import part_ranges
+
+    for M in (1, 7, 512, 32768, 1_572_864, 1_000_003):
+        for w in (1, 2, 3, 8, 16):
+            r = part_ranges(M, w)
+            assert r[0][0] == 0 and r[-1][1] == 8 * M
+            assert all(r[i][1] == r[i + 1][0] for i in range(w - 1))
+            assert all(a % 8 == 0 and b % 8 == 0 for a, b in r)
+
+
+def _relaxed_close_to_exact(bb, relaxed, exact, keys):
+    """SURVEY §8(a) relaxed tolerances against the exact build (as in the GPU
+    parity tests): no false negatives, FPR within 0.1 + 3 sigma in log2 over
+    2^24 negatives, mean load within 1 bit, variance within 15% (+3 sigma of
+    its estimate)."""
+    import math
+
+    assert relaxed.contains_many(keys).all(), "partitioned build: false negatives"
+    neg = bb.odd_keys(1 << 24, 12, device="cuda")
+    fp_e, fp_r = exact.count_hits(neg), relaxed.count_hits(neg)
+    sigma = math.sqrt(1 / max(fp_e, 1) + 1 / max(fp_r, 1)) / math.log(2)
+    assert abs(math.log2(max(fp_r, 1) / max(fp_e, 1))) <= 0.1 + 3 * sigma, (fp_e, fp_r)
+    h_r, h_e = bb.block_load_histogram(relaxed), bb.block_load_histogram(exact)
+    assert abs(h_r.mean_load - h_e.mean_load) <= 1.0
+    tol = 0.15 + 3 * math.sqrt(2.0 / relaxed.num_blocks)
+    assert abs(h_r.variance / h_e.variance - 1) <= tol, (h_r.variance, h_e.variance)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world,cfgkw,n", [
+    (1, dict(kind="blowchoc", k=14, choices=2, size_bits=16 * 2**20, seed=1), 2**20),
+    (2, dict(kind="blowchoc", k=14, choices=2, size_bits=16 * 2**20, seed=1), 2**20),
+    (3, dict(kind="blowchoc", k=14, choices=2, size_bits=16 * 2**20, seed=1), 2**20),
+    (4, dict(kind="blowchoc", k=16, choices=3, size_bits=16 * 300_007, seed=5), 300_007),
+    (8, dict(kind="blowchoc", k=11, choices=2, size_bits=2**26, seed=1), 5_000_000),
+    (16, dict(kind="blowchoc", k=8, choices=4, n_capacity=400_000, seed=9), 400_000),
+])
+def test_partitioned_insert_emulated_ranks(world, cfgkw, n):
+    """bc_insert_peers with W replicas held on one GPU (each rank's call
+    launched in turn with its key slice and every replica's address): each
+    block is written only in its owner's replica, and the owners' ranges put
+    together are a relaxed build of the whole stream within the stated
+    tolerance of the exact (reference-order) build."""
+    import ctypes
+
+    import paper_2501_18977_b200 as bb
+    from paper_2501_18977_b200 import _native
+    from paper_2501_18977_b200.distributed import part_ranges, slice_bounds
+
+    cfg = bb.FilterConfig(**cfgkw)
+    keys = bb.even_keys(n, 11, device="cuda")
+    exact = bb.Filter.from_config(cfg)
+    exact.insert_many(keys)
+    f = bb.Filter.from_config(cfg, insert_mode="relaxed")
+    nw = f.storage.d_words.numel()
+    reps = [torch.zeros(nw, dtype=torch.int64, device="cuda") for _ in range(world)]
+    ptrs = (ctypes.c_uint64 * world)(*[r.data_ptr() for r in reps])
+    stream = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    k64 = keys.view(torch.int64)
+    share = max(256, (f.num_blocks // 2) // world)
+    for rank, (lo, hi) in enumerate(slice_bounds(n, world)):
+        part = k64[lo:hi].contiguous()
+        _native.check(_native.lib().bc_insert_peers(
+            ctypes.c_void_p(f.handle), ptrs, world, ctypes.c_void_p(part.data_ptr()),
+            part.numel(), share, stream))
+    torch.cuda.synchronize()
+    ranges = part_ranges(f.num_blocks, world)
+    full = torch.zeros(nw, dtype=torch.int64, device="cuda")
+    for r, (a, b) in enumerate(ranges):
+        outside = torch.cat([reps[r][:a], reps[r][b:]])
+        assert not bool(outside.any()), f"replica {r} written outside its partition"
+        full[a:b] = reps[r][a:b]
+    f.storage.d_words.view(torch.int64).copy_(full)
+    f.storage.device_modified()
+    _relaxed_close_to_exact(bb, f, exact, keys)
+    with pytest.raises(RuntimeError):  # not a partitionable geometry (BC_EUNSUP)
+        g = bb.Filter.from_config(bb.FilterConfig(kind="blocked", k=8, n_capacity=1000, seed=1))
+        _native.check(_native.lib().bc_insert_peers(ctypes.c_void_p(g.handle), ptrs, world,
+                                                    ctypes.c_void_p(0), 0, 0, stream))
+
+
+def _partition_worker(rank, world, port):
+    import hashlib
+
+    import paper_2501_18977_b200 as bb
+    from paper_2501_18977_b200 import distributed as D
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    os.environ["BC_PEER_ALLREDUCE"] = "1"
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        cfg = bb.FilterConfig(kind="blowchoc", k=14, choices=2, size_bits=16 * 2**20, seed=1)
+        keys = bb.even_keys(2**20, 11, device="cuda")
+        pad = torch.empty(4096 + 192 * rank, dtype=torch.uint8, device="cuda")  # interior pointers
+        f = bb.Filter.from_config(cfg, insert_mode="relaxed")
+        assert D.build_partitioned(f, keys)
+        assert f.inserted == keys.numel()
+        digest = hashlib.sha256(f.storage.words.tobytes()).hexdigest()
+        seen = [None] * world
+        dist.all_gather_object(seen, digest)
+        assert len(set(seen)) == 1, "replicas differ after the partitioned build"
+        exact = bb.Filter.from_config(cfg)
+        exact.insert_many(keys)
+        _relaxed_close_to_exact(bb, f, exact, keys)
+        del pad
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_partitioned_build_two_processes_one_gpu():
+    """build_partitioned end to end: two ranks (gloo barriers) sharing cuda:0
+    map each other's replicas over CUDA IPC, each inserts its half of the
+    stream into the partitioned filter with one kernel, the owners' ranges
+    are broadcast, and both ranks end with the same relaxed build within
+    tolerance of the exact one."""
+    mp.spawn(_partition_worker, args=(2, free_port()), nprocs=2, join=True)
