@@ -91,7 +91,8 @@ cudaError_t launch_ordered_qgrams(const KParams &p, u64 *words, const u8 *seq, u
 // Exact stream-order insert of small filters as a dataflow (ordered_ticket.cu):
 // per-block tickets from a stable sort of (block, key) pairs, then keys commit
 // as soon as every earlier key sharing a block is done.  c in 2..8, 512-bit
-// blocks, random strategy, up to BC_TICKET_MAX_BLOCKS blocks (2^16).
+// blocks, random strategy, up to BC_TICKET_MAX_BLOCKS blocks (default 2^20,
+// 2^21 for c >= 3).
 bool ordered_ticket_supported(const KParams &p);
 cudaError_t launch_ordered_ticket(const KParams &p, u64 *words, const u64 *keys, u64 n,
                                   cudaStream_t s);

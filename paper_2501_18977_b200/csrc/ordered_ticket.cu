@@ -207,10 +207,18 @@ static u64 env_u64(const char *name, u64 dflt) {
 // order; BC_TICKET_CHUNK overrides, for tests).
 static u64 ticket_chunk() { return std::max<u64>(1, env_u64("BC_TICKET_CHUNK", 1ull << 24)); }
 
+// Filters up to 2^20 blocks (64 MiB), or 2^21 with three or more choices,
+// where claim rounds pay for many conflicts per round (measured, B200,
+// tools/ordered_probe.py bits:n:c:k at 14-16 bits per key: c = 2 at 2^18 /
+// 2^19 / 2^20 blocks 3843 / 4009 / 4152 vs 2174 / 2850 / 3188 Mkeys/s, at
+// 2^21 4148 vs 6017; c = 3 at 2^18 / 2^20 / 2^21 2026 / 1940 / 2376 vs
+// 604 / 927 / 1783).  BC_TICKET_MAX_BLOCKS overrides, BC_ORDERED_TICKET=0
+// disables.
 bool ordered_ticket_supported(const KParams &p) {
     if (!(p.fast_random && p.wpb == 8 && p.c >= 2 && p.c <= 8)) return false;
     if (env_u64("BC_ORDERED_TICKET", 1) == 0) return false;
-    return p.num_blocks <= env_u64("BC_TICKET_MAX_BLOCKS", 1ull << 16);
+    const u64 dflt = p.c >= 3 ? (1ull << 21) : (1ull << 20);
+    return p.num_blocks <= env_u64("BC_TICKET_MAX_BLOCKS", dflt);
 }
 
 template <int C, class Src>

@@ -25,10 +25,17 @@ CFGS = {
 }
 
 
+def spec(a: str):
+    """A BASELINE config number, or bits:n:c:k for another geometry."""
+    if ":" in a:
+        bits, n, c, k = (int(v) for v in a.split(":"))
+        return a, (dict(kind="blowchoc", k=k, choices=c, size_bits=bits, seed=1), n, None)
+    return int(a), CFGS[int(a)]
+
+
 def main():
-    cfgs = [int(a) for a in sys.argv[1:]] or [1]
-    for c in cfgs:
-        kw, n, want = CFGS[c]
+    cfgs = [spec(a) for a in sys.argv[1:]] or [spec("1")]
+    for c, (kw, n, want) in cfgs:
         if c == 3:
             want = json.load(open(os.path.join(ROOT, "tests/golden/fullsize_cfg3.json")))["words_sha256"]
         f = bb.Filter.from_config(bb.FilterConfig(**kw))
