@@ -11,8 +11,12 @@ run unmodified, in a fresh interpreter, through the GPU kernels:
   blocked, blowchoc c = 2/3, distinct, 16-bit toy blocks, shards);
 * test_acceptance.py C9 (toy-scale oracle agreement, :179-232) and C11
   (threaded sharded builds + BWCH round trips, :260-279);
-* test_filters.py, test_sharding.py, test_io.py, test_analysis.py: every
-  other reference test that reaches insert_many / contains_many.
+* test_filters.py, test_sharding.py, test_io.py, test_analysis.py and
+  test_cli.py (the reference's own CLI; its in-process cases go through the
+  binding, the two that spawn `python -m blowchoc.cli` run the reference's
+  numba path in the child): every other reference test that reaches
+  insert_many / contains_many; test_blockstore.py and test_hashing.py run
+  alongside.
 
 The binding records how many calls each GPU entry point served; the test
 requires both the insert and the lookup entry points to have been used.
@@ -66,5 +70,6 @@ def test_reference_acceptance_c9_c11_through_libbbchoc(tmp_path):
 
 def test_reference_filter_suites_through_libbbchoc(tmp_path):
     out, calls = run_reference_tests(
-        tmp_path, ["test_filters.py", "test_sharding.py", "test_io.py", "test_analysis.py"])
+        tmp_path, ["test_filters.py", "test_sharding.py", "test_io.py", "test_analysis.py",
+                   "test_cli.py", "test_blockstore.py", "test_hashing.py"])
     assert calls["insert_blocks"] > 0 and calls["contains_blocks"] > 0, calls
