@@ -571,6 +571,9 @@ __global__ void __launch_bounds__(256) ordered_window_kernel(
 #ifndef BC_ORD_UNR
 #define BC_ORD_UNR 0  // keys per load step of the commit (0: relaxed_unroll(C))
 #endif
+#ifndef BC_ORD_NT
+#define BC_ORD_NT 256  // threads per CTA of the claim rounds
+#endif
 #ifndef BC_ORD_DYN
 #define BC_ORD_DYN 1  // claim rounds: tiles after each warp's first taken from a CTA counter
 #endif
@@ -596,12 +599,12 @@ __global__ void __launch_bounds__(256) ordered_window_kernel(
 // state (u32 x 8, zeroed before each launch): [0..2] rotating round words
 // (pending total | exhausted << 31), [4..5] the u64 stream cursor.
 template <int C, class Src>
-__global__ void __launch_bounds__(kTPB, BC_ORD_MINB) ordered512_kernel(
+__global__ void __launch_bounds__(BC_ORD_NT, BC_ORD_MINB) ordered512_kernel(
     const __grid_constant__ KParams p, u64 *__restrict__ words, const Src src, u64 n, u32 cap,
     u32 *__restrict__ owner, u64 slots, u32 slot_shift, u32 *__restrict__ state,
     unsigned long long *__restrict__ admitted) {
     cg::grid_group grid = cg::this_grid();
-    __shared__ WarpSmem<C> smem[kWarps];
+    __shared__ WarpSmem<C> smem[BC_ORD_NT / 32];
     __shared__ u32 s_cnt, s_pend, s_adm, s_exh, s_tile;
     __shared__ u64 s_start;
     extern __shared__ __align__(16) unsigned char dsm[];
@@ -634,7 +637,7 @@ __global__ void __launch_bounds__(kTPB, BC_ORD_MINB) ordered512_kernel(
             s_adm = (free && st < n) ? (u32)min((u64)free, n - st) : 0u;
             s_exh = free && st + free >= n;
             s_cnt = 0;
-            s_tile = kTPB;  // tiles past the first one per warp, handed out on demand
+            s_tile = BC_ORD_NT;  // tiles past each warp's first, handed out on demand
             if (blockIdx.x == 0) state[(round + 1u) % 3u] = 0;  // last read in round r-1
         }
         __syncthreads();
@@ -692,7 +695,7 @@ __global__ void __launch_bounds__(kTPB, BC_ORD_MINB) ordered512_kernel(
 #if BC_ORD_DYN
             const u32 t1 = next_tile();
 #else
-            const u32 t1 = t0 + kTPB;
+            const u32 t1 = t0 + BC_ORD_NT;
 #endif
             u32 li_n = 0;
             u64 x_n = 0;
@@ -1224,7 +1227,7 @@ static cudaError_t launch_window(const KParams &p, u64 *words, const Src *src, c
     e = cudaMemsetAsync(state, 0, 8 * sizeof(u32), s);  // round words, cursor
     if (e != cudaSuccess) return e;
     const int sms = (int)sm_count();
-    u64 ctas = std::max<u64>(1, std::min<u64>((u64)sms * BC_ORD_MINB, chunk / 256));
+    u64 ctas = std::max<u64>(1, std::min<u64>((u64)sms * BC_ORD_MINB, chunk / BC_ORD_NT));
     u32 cap = 0;
     size_t smem = 0;
     for (int it = 0;; ++it) {
@@ -1235,7 +1238,7 @@ static cudaError_t launch_window(const KParams &p, u64 *words, const Src *src, c
             cudaSuccess)
             return cudaErrorInvalidValue;
         int per_sm = 0;
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fw, 256, smem) != cudaSuccess ||
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fw, BC_ORD_NT, smem) != cudaSuccess ||
             per_sm < 1)
             return cudaErrorInvalidConfiguration;
         if ((u64)per_sm * sms >= ctas) break;
@@ -1243,6 +1246,7 @@ static cudaError_t launch_window(const KParams &p, u64 *words, const Src *src, c
         ctas = (u64)per_sm * sms;  // fewer co-resident CTAs: larger lists, re-check
     }
     cfg.gridDim = dim3((unsigned)ctas);
+    cfg.blockDim = dim3(BC_ORD_NT);
     cfg.dynamicSmemBytes = smem;
     count_launch();
     switch (p.c) {
