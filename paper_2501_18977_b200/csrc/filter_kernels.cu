@@ -487,6 +487,33 @@ __device__ __forceinline__ bool ordered_check_cas(const KParams &p, u32 *own_cur
     return held;
 }
 
+// The CAS check split in two, so a tile's checks can be issued before the
+// previous tile's commit and consumed after it (BC_ORD_PIPE): issue returns
+// the old claim of every candidate slot (a repeated slot is not CASed again
+// and reports the key's own index: the first CAS answers for it).
+template <int C>
+__device__ __forceinline__ void ordered_cas_issue(const KParams &p, u32 *own_cur, u32 slot_shift,
+                                                  u64 x, u32 li, bool on, u32 (&old)[C]) {
+    u64 sl[C];
+#pragma unroll
+    for (int ci = 0; ci < C; ++ci) sl[ci] = owner_slot(block_index(p, x, ci), slot_shift);
+#pragma unroll
+    for (int ci = 0; ci < C; ++ci) {
+        bool dup = false;
+#pragma unroll
+        for (int cj = 0; cj < ci; ++cj) dup |= sl[cj] == sl[ci];
+        old[ci] = (on && !dup) ? atomicCAS(own_cur + sl[ci], li, kUnclaimed) : li;
+    }
+}
+
+template <int C>
+__device__ __forceinline__ bool ordered_cas_held(const u32 (&old)[C], u32 li) {
+    bool held = true;
+#pragma unroll
+    for (int ci = 0; ci < C; ++ci) held &= old[ci] == li;
+    return held;
+}
+
 __device__ __forceinline__ void ordered_claim(const KParams &p, u32 *own_nxt, u32 slot_shift,
                                               u64 x, u32 li) {
     for (u32 ci = 0; ci < p.c; ++ci)
@@ -580,6 +607,9 @@ __global__ void __launch_bounds__(256) ordered_window_kernel(
 #ifndef BC_ORD_CAS
 #define BC_ORD_CAS 1  // claim checks as one atomicCAS per distinct slot
 #endif
+#ifndef BC_ORD_PIPE
+#define BC_ORD_PIPE 1  // claim rounds: next tile's CAS checks issued before this tile's commit (cfg3 +1.8%, cfg5 +0.9%)
+#endif
 #ifndef BC_ORD_MINB
 #define BC_ORD_MINB 3  // <= 80 registers: 3 CTAs per SM (cfg3 +4%, cfg5 +8% over 2 CTAs at 102)
 #endif
@@ -672,12 +702,18 @@ __global__ void __launch_bounds__(BC_ORD_NT, BC_ORD_MINB) ordered512_kernel(
         u32 li = 0;
         u64 x = 0;
         bool valid = fetch(t0 + lane, li, x);
+#if BC_ORD_PIPE
+        u32 cas_old[C];
+        ordered_cas_issue<C>(p, own_cur, slot_shift, x, li, valid && t0 + lane < npend, cas_old);
+#endif
         while (t0 < total) {
 #ifdef BC_ORD_PROF
             const long long ta = clock64();
 #endif
             const u32 t = t0 + lane;
-#if BC_ORD_CAS
+#if BC_ORD_PIPE
+            const bool win = valid && t < npend && ordered_cas_held<C>(cas_old, li);
+#elif BC_ORD_CAS
             const bool win =
                 valid && t < npend && ordered_check_cas<C>(p, own_cur, slot_shift, x, li);
 #else
@@ -700,6 +736,12 @@ __global__ void __launch_bounds__(BC_ORD_NT, BC_ORD_MINB) ordered512_kernel(
             u32 li_n = 0;
             u64 x_n = 0;
             const bool valid_n = fetch(t1 + lane, li_n, x_n);
+#if BC_ORD_PIPE
+            // the next tile's checks are in flight during this tile's commit
+            u32 cas_n[C];
+            ordered_cas_issue<C>(p, own_cur, slot_shift, x_n, li_n, valid_n && t1 + lane < npend,
+                                 cas_n);
+#endif
 #ifdef BC_ORD_PROF
             const long long tc_ = clock64();
             t_rest += tc_ - tb_;
@@ -728,6 +770,10 @@ __global__ void __launch_bounds__(BC_ORD_NT, BC_ORD_MINB) ordered512_kernel(
             li = li_n;
             x = x_n;
             valid = valid_n;
+#if BC_ORD_PIPE
+#pragma unroll
+            for (int ci = 0; ci < C; ++ci) cas_old[ci] = cas_n[ci];
+#endif
             t0 = t1;
 #ifdef BC_ORD_PROF
             ++ntiles;

@@ -196,12 +196,230 @@ __global__ void __launch_bounds__(256) ticket_exec_kernel(
     }
 }
 
+// ---- version-tagged block records (BC_TICKET_REC_MAX_BLOCKS) ---------------------------------------
+// The hop from a key to its successor on a block above costs a fence after
+// the block store, the counter increment, the successor's poll, a fence and
+// the successor's block load: four L2 round trips on the critical path.  With
+// records, the block's words and its done-count travel together: block b is
+// kRecChunks 16-byte chunks, each three data words and the count as its tag.
+// A key polls its candidates' records until every chunk's tag equals its
+// ticket -- the data are then exactly the block after its predecessor -- and
+// publishes each candidate (the chosen one OR-ed with its mask, the others
+// as read) with the tag moved past its own ticket(s).  Each 16-byte chunk is
+// one aligned vector store and load, single-copy atomic in practice (the
+// assumption CUB's decoupled look-back makes for its 16-byte tile
+// descriptors), so a chunk is either wholly before or wholly after a
+// publication and no fences are needed: one store-to-load latency per hop.
+// Tags are cumulative over ticket sets (the rank kernel adds the tag a block
+// has when its set starts), so records are converted from and back to the
+// filter's words once per insert.
+constexpr int kRecChunks = 6;  // 16 data words in chunks of three
+
+__device__ __forceinline__ uint4 ld_relaxed_v4(const uint4 *p) {
+    uint4 v;
+    asm volatile("ld.relaxed.gpu.global.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "l"(p)
+                 : "memory");
+    return v;
+}
+
+__device__ __forceinline__ void st_relaxed_v4(uint4 *p, uint4 v) {
+    asm volatile("st.relaxed.gpu.global.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y),
+                 "r"(v.z), "r"(v.w)
+                 : "memory");
+}
+
+__global__ void __launch_bounds__(256) rec_from_words_kernel(const u32 *__restrict__ words, u64 M,
+                                                             uint4 *__restrict__ rec) {
+    const u64 stride = (u64)gridDim.x * blockDim.x;
+    for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < M * kRecChunks; i += stride) {
+        const u64 b = i / kRecChunks;
+        const u32 q = (u32)(i - b * kRecChunks), w0 = 3 * q;
+        const u32 *src = words + b * 16;
+        rec[i] = make_uint4(src[w0], w0 + 1 < 16 ? src[w0 + 1] : 0u, w0 + 2 < 16 ? src[w0 + 2] : 0u,
+                            0u);
+    }
+}
+
+__global__ void __launch_bounds__(256) rec_to_words_kernel(const uint4 *__restrict__ rec, u64 M,
+                                                           u32 *__restrict__ words) {
+    const u64 stride = (u64)gridDim.x * blockDim.x;
+    for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < M * 16; i += stride) {
+        const u64 b = i >> 4;
+        const u32 w = (u32)(i & 15u), q = w / 3, r = w - 3 * q;
+        const uint4 c = rec[b * kRecChunks + q];
+        words[i] = r == 0 ? c.x : (r == 1 ? c.y : c.z);
+    }
+}
+
+// ticket = rank in the set + the block's tag when the set starts
+__global__ void __launch_bounds__(256) ticket_rank_rec_kernel(const u32 *sblk, const u32 *spid,
+                                                              u64 m, const u32 *start, u64 M,
+                                                              const uint4 *rec, u32 *ticket) {
+    const u64 stride = (u64)gridDim.x * blockDim.x;
+    for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < m; i += stride) {
+        const u32 b = sblk[i];
+        ticket[spid[i]] = (u32)i - start[b] + (b < M ? rec[(u64)b * kRecChunks].w : 0u);
+    }
+}
+
+template <int C, class Src>
+__global__ void __launch_bounds__(256) ticket_rec_kernel(
+    const __grid_constant__ KParams p, uint4 *__restrict__ rec, const Src src, u64 n,
+    const u32 *__restrict__ ticket, u32 *__restrict__ tile_ctr,
+    unsigned long long *__restrict__ admitted) {
+    __shared__ u32 mcol[16][256];  // per-thread 512-bit mask columns
+    const u32 tid = threadIdx.x, lane = tid & 31;
+    u32 *col = &mcol[0][tid];
+    const u64 ntiles = (n + 31) / 32;
+    u32 n_adm = 0;
+    for (;;) {
+        u32 t = 0;
+        if (lane == 0) t = atomicAdd(tile_ctr, 1u);
+        t = __shfl_sync(kFull, t, 0);
+        if (t >= ntiles) break;
+        const u64 j = (u64)t * 32 + lane;
+        u64 x = 0;
+        const bool valid = j < n && src.admit(j, x);
+        n_adm += valid ? 1u : 0u;
+        u32 bl[C], want[C], nxt[C];
+        u32 first = 0;  // bit ci: ci is the first occurrence of its block
+        if (valid) {
+#pragma unroll
+            for (int ci = 0; ci < C; ++ci) {
+                bl[ci] = (u32)block_index(p, x, ci);
+                want[ci] = __ldg(ticket + j * C + ci);
+            }
+            // a block chosen m times by one key holds m consecutive tickets:
+            // wait for the first, publish past the last
+#pragma unroll
+            for (int ci = 0; ci < C; ++ci) {
+                u32 lo = want[ci], hi = want[ci];
+#pragma unroll
+                for (int cj = 0; cj < C; ++cj)
+                    if (bl[cj] == bl[ci]) {
+                        lo = min(lo, want[cj]);
+                        hi = max(hi, want[cj]);
+                    }
+                bool dup = false;
+#pragma unroll
+                for (int cj = 0; cj < ci; ++cj) dup |= bl[cj] == bl[ci];
+                first |= dup ? 0u : (1u << ci);
+                want[ci] = lo;
+                nxt[ci] = hi + 1;
+            }
+#pragma unroll
+            for (int w = 0; w < 16; ++w) col[w * 256] = 0u;
+            const u32 xlo = (u32)x, xhi = (u32)(x >> 32);
+            for (u32 i = 0; i < p.k; ++i) {
+                const u32 hi = mul_hi32(p.bit_a_lo[i], p.bit_a_hi[i], xlo, xhi);
+                atomicOr(&col[(hi >> 28) * 256], 1u << ((hi >> 23) & 31u));
+            }
+        }
+        bool pend = valid;
+        // per candidate: its record read and current (held until this key
+        // publishes: nobody else may advance it), or the predecessors still
+        // ahead of the key there as last seen.  Two or more ahead: only the
+        // tag of chunk 0 is polled (16 instead of 96 bytes), so keys queued
+        // deep behind others do not flood L2 with full-record polls.
+        uint4 d[C][kRecChunks];
+        u32 got = 0, far = 0;
+        while (__any_sync(kFull, pend)) {
+            if (pend) {
+#pragma unroll
+                for (int ci = 0; ci < C; ++ci)
+                    if (((first & ~got) >> ci) & 1u) {
+                        const uint4 *r = rec + (u64)bl[ci] * kRecChunks;
+                        if ((far >> ci) & 1u) {
+                            const u32 tag = ld_relaxed_v4(r).w;
+                            far = want[ci] - tag >= 2u ? far : far & ~(1u << ci);
+                        } else {
+                            bool ok = true;
+#pragma unroll
+                            for (int q = 0; q < kRecChunks; ++q) {
+                                d[ci][q] = ld_relaxed_v4(r + q);
+                                ok &= d[ci][q].w == want[ci];
+                            }
+                            got |= ok ? (1u << ci) : 0u;
+                            far |= (!ok && want[ci] - d[ci][0].w >= 2u) ? (1u << ci) : 0u;
+                        }
+                    }
+                if ((got & first) == first) {
+                    u32 m[18];
+#pragma unroll
+                    for (int w = 0; w < 16; ++w) m[w] = col[w * 256];
+                    m[16] = m[17] = 0u;
+                    bool noop = false;
+                    int best = 0;
+                    u32 best_r = 0xffffffffu;
+#pragma unroll
+                    for (int ci = 0; ci < C; ++ci) {
+                        // a repeated block: the data of its first occurrence
+                        int src_ci = ci;
+#pragma unroll
+                        for (int cj = C - 1; cj >= 0; --cj)
+                            if (cj < ci && bl[cj] == bl[ci]) src_ci = cj;
+                        u32 jj = 0, pres = 0;
+#pragma unroll
+                        for (int q = 0; q < kRecChunks; ++q) {
+                            uint4 w = d[0][q];
+#pragma unroll
+                            for (int cs = 1; cs < C; ++cs)
+                                if (cs == src_ci) w = d[cs][q];
+                            jj += __popc(w.x | m[3 * q]) + __popc(w.y | m[3 * q + 1]) +
+                                  __popc(w.z | m[3 * q + 2]);
+                            pres += __popc(w.x) + __popc(w.y) + __popc(w.z);
+                        }
+                        noop |= jj == pres;
+                        const u32 r = __ldg(p.rank + jj * (p.k + 1) + (jj - pres));
+                        if (r < best_r) {
+                            best_r = r;
+                            best = ci;
+                        }
+                    }
+                    // the chosen block is the first occurrence of its id
+                    u32 chosen = bl[best];
+#pragma unroll
+                    for (int ci = 0; ci < C; ++ci)
+                        if ((first >> ci) & 1u) {
+                            const bool orit = !noop && bl[ci] == chosen;
+#pragma unroll
+                            for (int q = 0; q < kRecChunks; ++q) {
+                                const uint4 w = d[ci][q];
+                                st_relaxed_v4(rec + (u64)bl[ci] * kRecChunks + q,
+                                              orit ? make_uint4(w.x | m[3 * q], w.y | m[3 * q + 1],
+                                                                w.z | m[3 * q + 2], nxt[ci])
+                                                   : make_uint4(w.x, w.y, w.z, nxt[ci]));
+                            }
+                        }
+                    pend = false;
+                }
+            }
+#if BC_TICKET_SLEEP
+            if (__any_sync(kFull, pend)) __nanosleep(BC_TICKET_SLEEP);
+#endif
+        }
+    }
+    if (Src::kCounts && admitted != nullptr) {
+        for (int o = 16; o > 0; o >>= 1) n_adm += __shfl_xor_sync(kFull, n_adm, o);
+        if (lane == 0 && n_adm) atomicAdd(admitted, (unsigned long long)n_adm);
+    }
+}
+
 // ---- host side -------------------------------------------------------------------------
 
 static u64 env_u64(const char *name, u64 dflt) {
     const char *e = std::getenv(name);
     return e ? std::strtoull(e, nullptr, 10) : dflt;
 }
+
+// Filters up to this many blocks run the ticket execution over version-tagged
+// records (ticket_rec_kernel): there the chains of dependent keys set the
+// rate, and a record hop is one store-to-load latency.  Above it the
+// execution is throughput-bound and the records' wider polls and full
+// rewrites of every candidate cost more than they save (BC_TICKET_REC_MAX_BLOCKS).
+static u64 ticket_rec_max_blocks() { return env_u64("BC_TICKET_REC_MAX_BLOCKS", 1ull << 18); }
 
 // Keys per ticket set (tickets are ranks within one set; sets run in stream
 // order; BC_TICKET_CHUNK overrides, for tests).
@@ -236,6 +454,18 @@ static cudaError_t exec_launch(const KParams &p, u64 *words, const Src &src, u64
     return cudaGetLastError();
 }
 
+template <int C, class Src>
+static cudaError_t rec_launch(const KParams &p, uint4 *rec, const Src &src, u64 n,
+                              const u32 *ticket, u32 *ctr, unsigned long long *admitted,
+                              cudaStream_t s) {
+    const void *fn = (const void *)ticket_rec_kernel<C, Src>;
+    const u64 inflight = std::max<u64>(256, p.num_blocks * env_u64("BC_TICKET_INFLIGHT_PCT", 100) / 100);
+    const unsigned grid = grid_for(fn, 256, 0, std::min<u64>((n + 255) / 256, (inflight + 255) / 256));
+    ticket_rec_kernel<C, Src><<<grid, 256, 0, s>>>(p, rec, src, n, ticket, ctr, admitted);
+    count_launch();
+    return cudaGetLastError();
+}
+
 template <class Src>
 static cudaError_t ticket_insert(const KParams &p, u64 *words, const Src &src, u64 n,
                                  unsigned long long *admitted, cudaStream_t s) {
@@ -249,16 +479,27 @@ static cudaError_t ticket_insert(const KParams &p, u64 *words, const Src &src, u
     cub::DeviceRadixSort::SortPairs(nullptr, cub_bytes, (const u32 *)nullptr, (u32 *)nullptr,
                                     (const u32 *)nullptr, (u32 *)nullptr, (int)m, 0, bits, s);
     // scratch: blk in/out, pid in/out, ticket (m each), start + done (M + 1 each), counter
+    // (records: M x kRecChunks x 16 bytes after the cub scratch)
     const size_t words32 = 5 * m + 2 * (M + 1) + 1;
     const size_t cub_off = ((words32 * 4 + 255) / 256) * 256;
+    const size_t rec_off = ((cub_off + cub_bytes + 255) / 256) * 256;
+    const bool use_rec = M <= ticket_rec_max_blocks();
+    const size_t rec_bytes = use_rec ? (size_t)M * kRecChunks * 16 : 0;
     unsigned char *scratch = nullptr;
-    cudaError_t e = cudaMallocAsync((void **)&scratch, cub_off + cub_bytes, s);
+    cudaError_t e = cudaMallocAsync((void **)&scratch, rec_off + rec_bytes, s);
     if (e != cudaSuccess) return e;
     u32 *blk = reinterpret_cast<u32 *>(scratch), *sblk = blk + m, *pid = sblk + m,
         *spid = pid + m, *ticket = spid + m, *start = ticket + m, *done = start + (M + 1),
         *ctr = done + (M + 1);
     void *cub_tmp = scratch + cub_off;
+    uint4 *rec = reinterpret_cast<uint4 *>(scratch + rec_off);
     const KParams &kp = p;
+    if (use_rec) {
+        const unsigned g = grid_for((const void *)rec_from_words_kernel, 256, 0,
+                                    (M * kRecChunks + 255) / 256);
+        rec_from_words_kernel<<<g, 256, 0, s>>>(reinterpret_cast<const u32 *>(words), M, rec);
+        count_launch();
+    }
     for (u64 off = 0; off < n && e == cudaSuccess; off += per) {
         const u64 len = std::min(per, n - off);
         const u64 ml = len * c;
@@ -274,18 +515,31 @@ static cudaError_t ticket_insert(const KParams &p, u64 *words, const Src &src, u
         if (e != cudaSuccess) break;
         const unsigned g2 = grid_for((const void *)ticket_runs_kernel, 256, 0, (ml + 255) / 256);
         ticket_runs_kernel<<<g2, 256, 0, s>>>(sblk, ml, start);
-        ticket_rank_kernel<<<g2, 256, 0, s>>>(sblk, spid, ml, start, ticket);
+        if (use_rec)
+            ticket_rank_rec_kernel<<<g2, 256, 0, s>>>(sblk, spid, ml, start, M, rec, ticket);
+        else
+            ticket_rank_kernel<<<g2, 256, 0, s>>>(sblk, spid, ml, start, ticket);
         count_launch(2);
-        e = cudaMemsetAsync(done, 0, sizeof(u32) * (M + 2), s);  // done[] and the tile counter
+        e = use_rec ? cudaMemsetAsync(ctr, 0, sizeof(u32), s)
+                          : cudaMemsetAsync(done, 0, sizeof(u32) * (M + 2), s);  // done[] + counter
         if (e != cudaSuccess) break;
         switch (p.c) {
-#define BC_TK(cc) \
-    case cc: e = exec_launch<cc, Src>(kp, words, sub, len, ticket, done, ctr, admitted, s); break;
+#define BC_TK(cc)                                                                             \
+    case cc:                                                                                  \
+        e = use_rec ? rec_launch<cc, Src>(kp, rec, sub, len, ticket, ctr, admitted, s)        \
+                    : exec_launch<cc, Src>(kp, words, sub, len, ticket, done, ctr, admitted, s); \
+        break;
             BC_TK(2) BC_TK(3) BC_TK(4) BC_TK(5) BC_TK(6) BC_TK(7) BC_TK(8)
 #undef BC_TK
             default: e = cudaErrorInvalidValue;
         }
         if (e == cudaSuccess) e = cudaGetLastError();
+    }
+    if (use_rec && e == cudaSuccess) {
+        const unsigned g = grid_for((const void *)rec_to_words_kernel, 256, 0, (M * 16 + 255) / 256);
+        rec_to_words_kernel<<<g, 256, 0, s>>>(rec, M, reinterpret_cast<u32 *>(words));
+        count_launch();
+        e = cudaGetLastError();
     }
     cudaFreeAsync(scratch, s);
     return e;
