@@ -49,8 +49,14 @@ __device__ __forceinline__ DevHash load_hash(const DevHash *h) {
     return r;
 }
 
+// Candidate entry of a lane without a key (SKIP): relaxed_load reads nothing
+// for it.  Without it such lanes read block 0, and in tiles that mix keys and
+// holes (the exact-order rounds' winners and losers) every warp queues on
+// that one line's L2 slice.
+constexpr u32 kNoBlock = 0xffffffffu;
+
 // ---- phase 1: one lane per key ----------------------------------------------------
-template <int C>
+template <int C, bool SKIP = false>
 __device__ __forceinline__ void phase1(const KParams &p, u64 x, bool valid, WarpSmem<C> &ws,
                                        int lane) {
     u32 *col = &ws.mask[0][lane];
@@ -91,7 +97,8 @@ __device__ __forceinline__ void phase1(const KParams &p, u64 x, bool valid, Warp
         }
     }
 #pragma unroll
-    for (int ci = 0; ci < C; ++ci) ws.blk[ci][lane] = valid ? (u32)block_index(p, x, ci) : 0u;
+    for (int ci = 0; ci < C; ++ci)
+        ws.blk[ci][lane] = valid ? (u32)block_index(p, x, ci) : (SKIP ? kNoBlock : 0u);
 }
 
 __device__ __forceinline__ u32 popc4(uint4 v) {
@@ -161,10 +168,12 @@ __device__ __forceinline__ void relaxed_load(const WarpSmem<C> &ws, const A &a, 
 #pragma unroll
     for (int u = 0; u < UNR; ++u)
 #pragma unroll
-        for (int ci = 0; ci < C; ++ci)
-            w[u][ci] = ld_block_cg(reinterpret_cast<const uint4 *>(
-                                       a.block(ws.blk[ci][4 * g + p0 + u])) +
-                                   s);
+        for (int ci = 0; ci < C; ++ci) {
+            const u32 b = ws.blk[ci][4 * g + p0 + u];
+            w[u][ci] = make_uint4(0u, 0u, 0u, 0u);  // a hole: all-zero mask too, a no-op
+            if (b != kNoBlock)
+                w[u][ci] = ld_block_cg(reinterpret_cast<const uint4 *>(a.block(b)) + s);
+        }
 }
 
 template <int C, int UNR, class A = LocalWords>

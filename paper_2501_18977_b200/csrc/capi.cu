@@ -307,15 +307,19 @@ static int ensure_ordered_scratch(bc_filter *f, cudaStream_t s) {
     if (const char *e = std::getenv("BC_ORDERED_CHUNK")) chunk = std::strtoull(e, nullptr, 10);
     chunk = std::max<u64>(chunk, 256);
     chunk = std::min<u64>(chunk, 1ull << 24);
-    // Claim slots: one per block up to 2^23 blocks, else 2^23 slots with the
-    // blocks hashed onto them (spurious conflicts only delay commits).  Two
-    // arrays of 2^23 u32 claims are 64 MiB, inside the persisting L2
-    // set-aside (79 MiB on B200) the ordered launch puts them under.
-    // Measured (bench.py --insert-mode ordered, tiled commits): cfg5
-    // (M = 2^27) 4518 Mkeys/s with 2^23 slots vs 2810 with 2^24 (128 MiB, no
-    // window).  BC_ORDERED_SLOTS overrides (0 = one per block).
+    // Claim slots: one per block up to 2^22 blocks (2^23 for c >= 3), else
+    // that many slots with the blocks hashed onto them (spurious conflicts
+    // only delay commits).  The two u32 claim arrays (32 or 64 MiB) sit
+    // under a persisting L2 window sized to them.  Fewer slots mean more
+    // spurious conflicts but leave more of the L2 to the candidate blocks:
+    // measured with the fitted set-aside (tools/r2_claims_sweep*.sh), c = 2:
+    // cfg5 7 450 / 7 661 / 7 117 Mkeys/s at 2^21 / 2^22 / 2^23 slots, cfg4's
+    // geometry 7 569 at 2^22 vs 6 910 at 2^23; c = 3: cfg3 5 267 at 2^22 vs
+    // 6 140 at 2^23, a 2 GiB filter 5 312 vs 5 858.  2^24 slots (128 MiB)
+    // fall out of the L2 (round 1: 2 810 vs 4 518).  BC_ORDERED_SLOTS
+    // overrides (0 = one per block).
     u64 slots = M;
-    u64 want = 1ull << 23;
+    u64 want = f->kp.c == 2 ? 1ull << 22 : 1ull << 23;
     if (const char *e = std::getenv("BC_ORDERED_SLOTS")) want = std::strtoull(e, nullptr, 10);
     if (want) {
         u64 pow2 = 1;
@@ -332,9 +336,9 @@ static int ensure_ordered_scratch(bc_filter *f, cudaStream_t s) {
     cudaError_t e = cudaMalloc(&owner, sizeof(u64) * owner_words);
     if (e == cudaSuccess) e = cudaMalloc(&lists, sizeof(u32) * 2 * chunk);
     if (e == cudaSuccess) e = cudaMalloc(&lkeys, sizeof(u64) * 2 * chunk);
-    if (e == cudaSuccess) e = cudaMalloc(&state, sizeof(u32) * 8);
+    if (e == cudaSuccess) e = cudaMalloc(&state, sizeof(u32) * 16);
     if (e == cudaSuccess) e = cudaMemsetAsync(owner, 0xff, sizeof(u64) * owner_words, s);
-    if (e == cudaSuccess) e = cudaMemsetAsync(state, 0, sizeof(u32) * 8, s);
+    if (e == cudaSuccess) e = cudaMemsetAsync(state, 0, sizeof(u32) * 16, s);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&done, cudaEventDisableTiming);
     if (e != cudaSuccess) {
         cudaFree(owner);

@@ -514,6 +514,45 @@ __device__ __forceinline__ bool ordered_cas_held(const u32 (&old)[C], u32 li) {
     return held;
 }
 
+// Epoch-tagged claims (BC_ORD_TAG): a claim is (tag << 24 | li - base), the
+// tag falling by one every time an array is claimed into (every second
+// round) and base a lower bound of every index claiming that round.  A newer
+// round's claims are smaller than anything an older round left behind, so
+// atomicMin overwrites stale claims and nothing is ever reset: the check is
+// a plain load compared with the key's own value, not an atomicCAS.  Per key
+// that leaves c L2 atomics instead of 2c (the rounds queue on the L2 atomic
+// units, not on DRAM).  The arrays are cleared in-kernel when the 8-bit tag
+// wraps (every 512 rounds) and in a launch's first two rounds.
+constexpr u32 kRelBits = 24;
+constexpr u32 kRelLimit = (1u << kRelBits) - 1u;  // 0xffffffff is never a claim
+
+__device__ __forceinline__ u32 claim_tag(u32 round) {
+    return (255u - ((round >> 1) & 255u)) << kRelBits;
+}
+
+template <int C>
+__device__ __forceinline__ void ordered_tag_issue(const KParams &p, const u32 *own_cur,
+                                                  u32 slot_shift, u64 x, bool on, u32 (&old)[C]) {
+#pragma unroll
+    for (int ci = 0; ci < C; ++ci)
+        old[ci] = on ? __ldcg(own_cur + owner_slot(block_index(p, x, ci), slot_shift)) : kUnclaimed;
+}
+
+template <int C>
+__device__ __forceinline__ void ordered_claim_tag(const KParams &p, u32 *own_nxt, u32 slot_shift,
+                                                  u64 x, u32 v) {
+#pragma unroll
+    for (int ci = 0; ci < C; ++ci)
+        atomicMin(own_nxt + owner_slot(block_index(p, x, ci), slot_shift), v);
+}
+
+template <int C>
+__device__ __forceinline__ void ordered_prefetch(const KParams &p, const u64 *words, u64 x) {
+#pragma unroll
+    for (int ci = 0; ci < C; ++ci)
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(words + block_index(p, x, ci) * 8));
+}
+
 __device__ __forceinline__ void ordered_claim(const KParams &p, u32 *own_nxt, u32 slot_shift,
                                               u64 x, u32 li) {
     for (u32 ci = 0; ci < p.c; ++ci)
@@ -610,6 +649,15 @@ __global__ void __launch_bounds__(256) ordered_window_kernel(
 #ifndef BC_ORD_PIPE
 #define BC_ORD_PIPE 1  // claim rounds: next tile's CAS checks issued before this tile's commit (cfg3 +1.8%, cfg5 +0.9%)
 #endif
+#ifndef BC_ORD_TAG
+#define BC_ORD_TAG 0  // claim rounds: epoch-tagged claims checked with plain loads (measured slower)
+#endif
+#ifndef BC_ORD_SKIP
+#define BC_ORD_SKIP 1  // commit tiles: lanes without a winner read nothing (not block 0)
+#endif
+#ifndef BC_ORD_PF
+#define BC_ORD_PF 0  // L2 prefetch of candidate blocks: 1 with the next tile's checks, 2 at first claim, 3 both
+#endif
 #ifndef BC_ORD_MINB
 #define BC_ORD_MINB 3  // <= 80 registers: 3 CTAs per SM (cfg3 +4%, cfg5 +8% over 2 CTAs at 102)
 #endif
@@ -626,8 +674,10 @@ __global__ void __launch_bounds__(256) ordered_window_kernel(
 // slice reached the end of the stream (bit 31 of the same word: the cursor
 // itself cannot be compared after the sync, a fast CTA may already have
 // taken its next slice).
-// state (u32 x 8, zeroed before each launch): [0..2] rotating round words
-// (pending total | exhausted << 31), [4..5] the u64 stream cursor.
+// state (u32 x 16; [0..7] zeroed, [8..10] all-ones before each launch):
+// [0..2] rotating round words (pending total | exhausted << 31), [4..5] the
+// u64 stream cursor, [8..10] rotating minimum pending index (BC_ORD_TAG: the
+// next round's claim base).
 template <int C, class Src>
 __global__ void __launch_bounds__(BC_ORD_NT, BC_ORD_MINB) ordered512_kernel(
     const __grid_constant__ KParams p, u64 *__restrict__ words, const Src src, u64 n, u32 cap,
@@ -635,7 +685,7 @@ __global__ void __launch_bounds__(BC_ORD_NT, BC_ORD_MINB) ordered512_kernel(
     unsigned long long *__restrict__ admitted) {
     cg::grid_group grid = cg::this_grid();
     __shared__ WarpSmem<C> smem[BC_ORD_NT / 32];
-    __shared__ u32 s_cnt, s_pend, s_adm, s_exh, s_tile;
+    __shared__ u32 s_cnt, s_pend, s_adm, s_exh, s_tile, s_min;
     __shared__ u64 s_start;
     extern __shared__ __align__(16) unsigned char dsm[];
     WarpSmem<C> &ws = smem[threadIdx.x >> 5];
@@ -651,6 +701,9 @@ __global__ void __launch_bounds__(BC_ORD_NT, BC_ORD_MINB) ordered512_kernel(
     }
     u32 round = 0;
     u32 n_admitted = 0;
+#if BC_ORD_TAG
+    u32 base_cur = 0, base_prev = 0;  // claim bases of this round and the last
+#endif
 #ifdef BC_ORD_PROF
     long long t_work = 0, t_sync = 0, tq = clock64();
     long long t_chk = 0, t_com = 0, t_rest = 0;
@@ -659,6 +712,17 @@ __global__ void __launch_bounds__(BC_ORD_NT, BC_ORD_MINB) ordered512_kernel(
     for (;;) {
         u32 *own_cur = owner + (round & 1u) * slots;
         u32 *own_nxt = owner + ((round + 1u) & 1u) * slots;
+#if BC_ORD_TAG
+        if (((round >> 1) & 255u) == 0) {
+            // the tag restarts: whatever the array holds (last checked one
+            // round ago, or left by an earlier launch) would outrank it
+            for (u64 i = blockIdx.x * (u64)BC_ORD_NT + threadIdx.x; i < slots;
+                 i += (u64)gridDim.x * BC_ORD_NT)
+                __stcg(own_nxt + i, kUnclaimed);
+            grid.sync();
+        }
+        const u32 tag_cur = claim_tag(round), tag_prev = claim_tag(round - 1u);
+#endif
         if (threadIdx.x == 0) {
             // refill to cap from the stream (s_pend: this CTA's losers of last round)
             const u32 free = cap - s_pend;
@@ -667,8 +731,12 @@ __global__ void __launch_bounds__(BC_ORD_NT, BC_ORD_MINB) ordered512_kernel(
             s_adm = (free && st < n) ? (u32)min((u64)free, n - st) : 0u;
             s_exh = free && st + free >= n;
             s_cnt = 0;
+            s_min = kUnclaimed;
             s_tile = BC_ORD_NT;  // tiles past each warp's first, handed out on demand
-            if (blockIdx.x == 0) state[(round + 1u) % 3u] = 0;  // last read in round r-1
+            if (blockIdx.x == 0) {
+                state[(round + 1u) % 3u] = 0;  // last read in round r-1
+                state[8u + (round + 1u) % 3u] = kUnclaimed;
+            }
         }
         __syncthreads();
         const u32 npend = s_pend, total = s_pend + s_adm;
@@ -702,16 +770,29 @@ __global__ void __launch_bounds__(BC_ORD_NT, BC_ORD_MINB) ordered512_kernel(
         u32 li = 0;
         u64 x = 0;
         bool valid = fetch(t0 + lane, li, x);
-#if BC_ORD_PIPE
+#if BC_ORD_TAG
+        // a pending key claimed last round iff its index was within range of
+        // that round's base; its claim holds where the slot still shows it
+        u32 cas_old[C];
+        u32 rel = li - base_prev;
+        ordered_tag_issue<C>(p, own_cur, slot_shift, x,
+                             valid && t0 + lane < npend && rel < kRelLimit, cas_old);
+#elif BC_ORD_PIPE
         u32 cas_old[C];
         ordered_cas_issue<C>(p, own_cur, slot_shift, x, li, valid && t0 + lane < npend, cas_old);
+#endif
+#if BC_ORD_PF & 1
+        if (valid && t0 + lane < npend) ordered_prefetch<C>(p, words, x);
 #endif
         while (t0 < total) {
 #ifdef BC_ORD_PROF
             const long long ta = clock64();
 #endif
             const u32 t = t0 + lane;
-#if BC_ORD_PIPE
+#if BC_ORD_TAG
+            const bool win = valid && t < npend && rel < kRelLimit &&
+                             ordered_cas_held<C>(cas_old, tag_prev | rel);
+#elif BC_ORD_PIPE
             const bool win = valid && t < npend && ordered_cas_held<C>(cas_old, li);
 #elif BC_ORD_CAS
             const bool win =
@@ -720,13 +801,29 @@ __global__ void __launch_bounds__(BC_ORD_NT, BC_ORD_MINB) ordered512_kernel(
             const bool win = valid && t < npend && ordered_check(p, own_cur, slot_shift, x, li);
 #endif
             const bool lose = valid && !win;
+#if BC_ORD_TAG
+            // out of range of this round's base: stay pending without a claim
+            // (the next base is the oldest pending index, so range returns)
+            if (lose && li - base_cur < kRelLimit)
+                ordered_claim_tag<C>(p, own_nxt, slot_shift, x, tag_cur | (li - base_cur));
+#else
             if (lose) ordered_claim(p, own_nxt, slot_shift, x, li);
+#endif
+#if BC_ORD_PF & 2
+            if (valid && t >= npend) ordered_prefetch<C>(p, words, x);  // checked next round
+#endif
             const u32 lm = __ballot_sync(kFull, lose);
 #ifdef BC_ORD_PROF
             const long long tb_ = clock64();
             t_chk += tb_ - ta;
 #endif
             u32 base = 0;
+#if BC_ORD_TAG
+            if (lm) {
+                const u32 mn = __reduce_min_sync(kFull, lose ? li : kUnclaimed);
+                if (lane == 0) atomicMin(&s_min, mn);
+            }
+#endif
             if (lm && lane == 0) base = atomicAdd(&s_cnt, (u32)__popc(lm));
 #if BC_ORD_DYN
             const u32 t1 = next_tile();
@@ -736,18 +833,27 @@ __global__ void __launch_bounds__(BC_ORD_NT, BC_ORD_MINB) ordered512_kernel(
             u32 li_n = 0;
             u64 x_n = 0;
             const bool valid_n = fetch(t1 + lane, li_n, x_n);
-#if BC_ORD_PIPE
+#if BC_ORD_TAG
+            // the next tile's claim loads are in flight during this tile's commit
+            u32 cas_n[C];
+            const u32 rel_n = li_n - base_prev;
+            ordered_tag_issue<C>(p, own_cur, slot_shift, x_n,
+                                 valid_n && t1 + lane < npend && rel_n < kRelLimit, cas_n);
+#elif BC_ORD_PIPE
             // the next tile's checks are in flight during this tile's commit
             u32 cas_n[C];
             ordered_cas_issue<C>(p, own_cur, slot_shift, x_n, li_n, valid_n && t1 + lane < npend,
                                  cas_n);
+#endif
+#if BC_ORD_PF & 1
+            if (valid_n && t1 + lane < npend) ordered_prefetch<C>(p, words, x_n);
 #endif
 #ifdef BC_ORD_PROF
             const long long tc_ = clock64();
             t_rest += tc_ - tb_;
 #endif
             if (__ballot_sync(kFull, win)) {  // tiles of admitted keys only claim
-                phase1<C>(p, x, win, ws, lane);
+                phase1<C, BC_ORD_SKIP != 0>(p, x, win, ws, lane);
                 __syncwarp();
                 phase2<OP_INSERT, C, BC_ORD_UNR>(p, words, ws, lane);
                 __syncwarp();
@@ -770,7 +876,10 @@ __global__ void __launch_bounds__(BC_ORD_NT, BC_ORD_MINB) ordered512_kernel(
             li = li_n;
             x = x_n;
             valid = valid_n;
-#if BC_ORD_PIPE
+#if BC_ORD_TAG
+            rel = rel_n;
+#endif
+#if BC_ORD_PIPE || BC_ORD_TAG
 #pragma unroll
             for (int ci = 0; ci < C; ++ci) cas_old[ci] = cas_n[ci];
 #endif
@@ -782,6 +891,9 @@ __global__ void __launch_bounds__(BC_ORD_NT, BC_ORD_MINB) ordered512_kernel(
         __syncthreads();  // the round's local appends are complete
         if (threadIdx.x == 0) {
             s_pend = s_cnt;
+#if BC_ORD_TAG
+            if (s_cnt) atomicMin(state + 8u + round % 3u, s_min);
+#endif
             if (s_cnt) atomicAdd(state + round % 3u, s_cnt);
             if (s_exh) atomicOr(state + round % 3u, 0x80000000u);
         }
@@ -802,6 +914,15 @@ __global__ void __launch_bounds__(BC_ORD_NT, BC_ORD_MINB) ordered512_kernel(
 #endif
         const u32 rw = __ldcg(state + round % 3u);
         const bool more = (rw & 0x7fffffffu) != 0 || !(rw >> 31);
+#if BC_ORD_TAG
+        {
+            // every key that claims next round is pending now (index >= the
+            // minimum) or enters later (index above every pending one)
+            const u32 mp = __ldcg(state + 8u + round % 3u);
+            base_prev = base_cur;
+            if (mp != kUnclaimed) base_cur = mp;
+        }
+#endif
         u32 *tmp = cur;
         cur = nxt;
         nxt = tmp;
@@ -920,6 +1041,7 @@ struct L2Info {
     size_t l2 = 0, persist = 0, window = 0;
     bool init = false;
     bool on = false;  // persisting set-aside carved out on this device
+    size_t limit = 0;  // its current size
 };
 
 constexpr int kMaxDevices = 64;
@@ -973,7 +1095,10 @@ static void l2_release_locked(L2Info &i) {
 }
 
 // Window for a filter of fbytes on the current device, or false.
-static bool l2_window(size_t fbytes, size_t *bytes, float *hit_ratio) {
+// `fit`: carve out no more than the window needs (the rest of the L2 stays
+// with everything else the kernel touches) instead of the device maximum.
+static bool l2_window(size_t fbytes, size_t *bytes, float *hit_ratio, bool fit = false,
+                      size_t cap = 0) {
     const int mode = l2_persist_mode();
     std::lock_guard<std::mutex> lk(g_l2_mu);
     L2Info *i = l2_info_locked(current_device());
@@ -983,15 +1108,19 @@ static bool l2_window(size_t fbytes, size_t *bytes, float *hit_ratio) {
         l2_release_locked(*i);
         return false;
     }
-    if (!i->on) {
-        if (cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, i->persist) != cudaSuccess) {
+    size_t limit = fit ? std::min(i->persist, (fbytes + (1u << 20) - 1) & ~(size_t)((1u << 20) - 1))
+                       : i->persist;
+    if (cap) limit = std::min(limit, cap);
+    if (!i->on || i->limit != limit) {
+        if (cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, limit) != cudaSuccess) {
             cudaGetLastError();
             return false;
         }
         i->on = true;
+        i->limit = limit;
     }
     *bytes = std::min(fbytes, i->window);
-    *hit_ratio = std::min(1.0f, (float)i->persist / (float)std::max<size_t>(*bytes, 1));
+    *hit_ratio = std::min(1.0f, (float)limit / (float)std::max<size_t>(*bytes, 1));
     return true;
 }
 
@@ -1252,7 +1381,20 @@ static cudaError_t launch_window(const KParams &p, u64 *words, const Src *src, c
     size_t bytes = 0;
     float hit = 0.f;
     const size_t claim_bytes = sizeof(u32) * 2 * slots;
-    if (l2_window(claim_bytes, &bytes, &hit)) {
+    // The set-aside is sized to the claims, not to the device maximum: what
+    // it takes beyond them is lost to the candidate blocks and the dirty
+    // lines of the commits (B200: cfg3 5 395 -> 6 140 Mkeys/s, cfg5 with 2^22
+    // slots 5 986 -> 7 661; BC_ORDERED_PERSIST_FIT=0 restores the maximum,
+    // BC_ORDERED_PERSIST_MB caps it).
+    static const bool fit = [] {
+        const char *e = getenv("BC_ORDERED_PERSIST_FIT");
+        return e == nullptr || atoi(e) != 0;
+    }();
+    static const size_t cap_mb = [] {
+        const char *e = getenv("BC_ORDERED_PERSIST_MB");
+        return e ? (size_t)atoi(e) : (size_t)0;
+    }();
+    if (l2_window(claim_bytes, &bytes, &hit, fit, cap_mb << 20)) {
         attr[1].id = cudaLaunchAttributeAccessPolicyWindow;
         attr[1].val.accessPolicyWindow.base_ptr = owner;
         attr[1].val.accessPolicyWindow.num_bytes = bytes;
@@ -1271,6 +1413,7 @@ static cudaError_t launch_window(const KParams &p, u64 *words, const Src *src, c
     // the window is spread over as many co-resident CTAs as fit, at least
     // 256 entries per CTA
     e = cudaMemsetAsync(state, 0, 8 * sizeof(u32), s);  // round words, cursor
+    if (e == cudaSuccess) e = cudaMemsetAsync(state + 8, 0xff, 8 * sizeof(u32), s);  // minima
     if (e != cudaSuccess) return e;
     const int sms = (int)sm_count();
     u64 ctas = std::max<u64>(1, std::min<u64>((u64)sms * BC_ORD_MINB, chunk / BC_ORD_NT));
