@@ -303,23 +303,26 @@ static int ensure_ordered_scratch(bc_filter *f, cudaStream_t s) {
     // is best at M/2 (550 Mkeys/s vs 515 at 2M, 440 at M/4); cfg3 (M = 2^23)
     // at 2^19 (1765 vs 1602 at 2^20, 442 at 2^22); cfg5 (M = 2^27) 1781 at
     // 2^18, 1896 at 2^20.
-    u64 chunk = std::min<u64>(M / 2, 1ull << 19);
+    // One-array rounds (ordered1_kernel, tools/r2_one_sweep.sh): cfg3 (c = 3)
+    // 7 262 / 7 307 / 6 408 Mkeys/s at 3*2^17 / 2^19 / 3*2^18; cfg5 (c = 2)
+    // 8 551 / 8 875 / 9 111.
+    u64 chunk = std::min<u64>(M / 2, (ordered_one() && f->kp.c == 2) ? 3ull << 18 : 1ull << 19);
     if (const char *e = std::getenv("BC_ORDERED_CHUNK")) chunk = std::strtoull(e, nullptr, 10);
     chunk = std::max<u64>(chunk, 256);
     chunk = std::min<u64>(chunk, 1ull << 24);
-    // Claim slots: one per block up to 2^22 blocks (2^23 for c >= 3), else
-    // that many slots with the blocks hashed onto them (spurious conflicts
-    // only delay commits).  The two u32 claim arrays (32 or 64 MiB) sit
-    // under a persisting L2 window sized to them.  Fewer slots mean more
-    // spurious conflicts but leave more of the L2 to the candidate blocks:
-    // measured with the fitted set-aside (tools/r2_claims_sweep*.sh), c = 2:
-    // cfg5 7 450 / 7 661 / 7 117 Mkeys/s at 2^21 / 2^22 / 2^23 slots, cfg4's
-    // geometry 7 569 at 2^22 vs 6 910 at 2^23; c = 3: cfg3 5 267 at 2^22 vs
-    // 6 140 at 2^23, a 2 GiB filter 5 312 vs 5 858.  2^24 slots (128 MiB)
-    // fall out of the L2 (round 1: 2 810 vs 4 518).  BC_ORDERED_SLOTS
-    // overrides (0 = one per block).
+    // Claim slots: one per block up to 2^23 blocks, else 2^23 slots with the
+    // blocks hashed onto them (spurious conflicts only delay commits).  The
+    // claims (one u32 array of 32 MiB for ordered1_kernel) sit under a
+    // persisting L2 window sized to them.  Fewer slots mean more spurious
+    // conflicts, more take the L2 from the candidate blocks
+    // (tools/r2_one_sweep.sh, Mkeys/s at 2^22 / 2^23 / 2^24 slots: cfg5
+    // 8 810 / 8 875 / 7 909, cfg4's geometry 8 821 / 9 075 / 7 892; a 2 GiB
+    // c = 3 filter 6 901 at 2^23, 6 769 at 2^24).  The two-array rounds
+    // (BC_ORDERED_ONE=0, 8 bytes per slot) are best at 2^22 slots for c = 2
+    // (cfg5 7 661 vs 7 117 at 2^23) and 2^23 for c >= 3 (cfg3 6 140 vs
+    // 5 267).  BC_ORDERED_SLOTS overrides (0 = one per block).
     u64 slots = M;
-    u64 want = f->kp.c == 2 ? 1ull << 22 : 1ull << 23;
+    u64 want = (!ordered_one() && f->kp.c == 2) ? 1ull << 22 : 1ull << 23;
     if (const char *e = std::getenv("BC_ORDERED_SLOTS")) want = std::strtoull(e, nullptr, 10);
     if (want) {
         u64 pow2 = 1;

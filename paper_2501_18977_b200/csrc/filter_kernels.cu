@@ -514,21 +514,17 @@ __device__ __forceinline__ bool ordered_cas_held(const u32 (&old)[C], u32 li) {
     return held;
 }
 
-// Epoch-tagged claims (BC_ORD_TAG): a claim is (tag << 24 | li - base), the
-// tag falling by one every time an array is claimed into (every second
-// round) and base a lower bound of every index claiming that round.  A newer
-// round's claims are smaller than anything an older round left behind, so
-// atomicMin overwrites stale claims and nothing is ever reset: the check is
-// a plain load compared with the key's own value, not an atomicCAS.  Per key
-// that leaves c L2 atomics instead of 2c (the rounds queue on the L2 atomic
-// units, not on DRAM).  The arrays are cleared in-kernel when the 8-bit tag
-// wraps (every 512 rounds) and in a launch's first two rounds.
+// Epoch-tagged claims (ordered1_kernel): a claim is (tag << 24 | li - base),
+// the tag falling by one every round and base a lower bound of every index
+// claiming that round.  A newer round's claims are smaller than anything an
+// older round left behind, so atomicMin overwrites stale claims and nothing
+// is ever reset: the check is a plain load compared with the key's own value.
+// The array is cleared in-kernel when the 8-bit tag wraps (every 256 rounds)
+// and in a launch's first round.
 constexpr u32 kRelBits = 24;
 constexpr u32 kRelLimit = (1u << kRelBits) - 1u;  // 0xffffffff is never a claim
 
-__device__ __forceinline__ u32 claim_tag(u32 round) {
-    return (255u - ((round >> 1) & 255u)) << kRelBits;
-}
+__device__ __forceinline__ u32 claim_tag(u32 round) { return (255u - (round & 255u)) << kRelBits; }
 
 template <int C>
 __device__ __forceinline__ void ordered_tag_issue(const KParams &p, const u32 *own_cur,
@@ -649,9 +645,6 @@ __global__ void __launch_bounds__(256) ordered_window_kernel(
 #ifndef BC_ORD_PIPE
 #define BC_ORD_PIPE 1  // claim rounds: next tile's CAS checks issued before this tile's commit (cfg3 +1.8%, cfg5 +0.9%)
 #endif
-#ifndef BC_ORD_TAG
-#define BC_ORD_TAG 0  // claim rounds: epoch-tagged claims checked with plain loads (measured slower)
-#endif
 #ifndef BC_ORD_SKIP
 #define BC_ORD_SKIP 1  // commit tiles: lanes without a winner read nothing (not block 0)
 #endif
@@ -674,10 +667,9 @@ __global__ void __launch_bounds__(256) ordered_window_kernel(
 // slice reached the end of the stream (bit 31 of the same word: the cursor
 // itself cannot be compared after the sync, a fast CTA may already have
 // taken its next slice).
-// state (u32 x 16; [0..7] zeroed, [8..10] all-ones before each launch):
+// state (u32 x 16; [0..7] zeroed, [8..15] all-ones before each launch):
 // [0..2] rotating round words (pending total | exhausted << 31), [4..5] the
-// u64 stream cursor, [8..10] rotating minimum pending index (BC_ORD_TAG: the
-// next round's claim base).
+// u64 stream cursor ([8..10] belong to ordered1_kernel).
 template <int C, class Src>
 __global__ void __launch_bounds__(BC_ORD_NT, BC_ORD_MINB) ordered512_kernel(
     const __grid_constant__ KParams p, u64 *__restrict__ words, const Src src, u64 n, u32 cap,
@@ -685,7 +677,7 @@ __global__ void __launch_bounds__(BC_ORD_NT, BC_ORD_MINB) ordered512_kernel(
     unsigned long long *__restrict__ admitted) {
     cg::grid_group grid = cg::this_grid();
     __shared__ WarpSmem<C> smem[BC_ORD_NT / 32];
-    __shared__ u32 s_cnt, s_pend, s_adm, s_exh, s_tile, s_min;
+    __shared__ u32 s_cnt, s_pend, s_adm, s_exh, s_tile;
     __shared__ u64 s_start;
     extern __shared__ __align__(16) unsigned char dsm[];
     WarpSmem<C> &ws = smem[threadIdx.x >> 5];
@@ -701,9 +693,6 @@ __global__ void __launch_bounds__(BC_ORD_NT, BC_ORD_MINB) ordered512_kernel(
     }
     u32 round = 0;
     u32 n_admitted = 0;
-#if BC_ORD_TAG
-    u32 base_cur = 0, base_prev = 0;  // claim bases of this round and the last
-#endif
 #ifdef BC_ORD_PROF
     long long t_work = 0, t_sync = 0, tq = clock64();
     long long t_chk = 0, t_com = 0, t_rest = 0;
@@ -712,17 +701,6 @@ __global__ void __launch_bounds__(BC_ORD_NT, BC_ORD_MINB) ordered512_kernel(
     for (;;) {
         u32 *own_cur = owner + (round & 1u) * slots;
         u32 *own_nxt = owner + ((round + 1u) & 1u) * slots;
-#if BC_ORD_TAG
-        if (((round >> 1) & 255u) == 0) {
-            // the tag restarts: whatever the array holds (last checked one
-            // round ago, or left by an earlier launch) would outrank it
-            for (u64 i = blockIdx.x * (u64)BC_ORD_NT + threadIdx.x; i < slots;
-                 i += (u64)gridDim.x * BC_ORD_NT)
-                __stcg(own_nxt + i, kUnclaimed);
-            grid.sync();
-        }
-        const u32 tag_cur = claim_tag(round), tag_prev = claim_tag(round - 1u);
-#endif
         if (threadIdx.x == 0) {
             // refill to cap from the stream (s_pend: this CTA's losers of last round)
             const u32 free = cap - s_pend;
@@ -731,12 +709,8 @@ __global__ void __launch_bounds__(BC_ORD_NT, BC_ORD_MINB) ordered512_kernel(
             s_adm = (free && st < n) ? (u32)min((u64)free, n - st) : 0u;
             s_exh = free && st + free >= n;
             s_cnt = 0;
-            s_min = kUnclaimed;
             s_tile = BC_ORD_NT;  // tiles past each warp's first, handed out on demand
-            if (blockIdx.x == 0) {
-                state[(round + 1u) % 3u] = 0;  // last read in round r-1
-                state[8u + (round + 1u) % 3u] = kUnclaimed;
-            }
+            if (blockIdx.x == 0) state[(round + 1u) % 3u] = 0;  // last read in round r-1
         }
         __syncthreads();
         const u32 npend = s_pend, total = s_pend + s_adm;
@@ -770,14 +744,7 @@ __global__ void __launch_bounds__(BC_ORD_NT, BC_ORD_MINB) ordered512_kernel(
         u32 li = 0;
         u64 x = 0;
         bool valid = fetch(t0 + lane, li, x);
-#if BC_ORD_TAG
-        // a pending key claimed last round iff its index was within range of
-        // that round's base; its claim holds where the slot still shows it
-        u32 cas_old[C];
-        u32 rel = li - base_prev;
-        ordered_tag_issue<C>(p, own_cur, slot_shift, x,
-                             valid && t0 + lane < npend && rel < kRelLimit, cas_old);
-#elif BC_ORD_PIPE
+#if BC_ORD_PIPE
         u32 cas_old[C];
         ordered_cas_issue<C>(p, own_cur, slot_shift, x, li, valid && t0 + lane < npend, cas_old);
 #endif
@@ -789,10 +756,7 @@ __global__ void __launch_bounds__(BC_ORD_NT, BC_ORD_MINB) ordered512_kernel(
             const long long ta = clock64();
 #endif
             const u32 t = t0 + lane;
-#if BC_ORD_TAG
-            const bool win = valid && t < npend && rel < kRelLimit &&
-                             ordered_cas_held<C>(cas_old, tag_prev | rel);
-#elif BC_ORD_PIPE
+#if BC_ORD_PIPE
             const bool win = valid && t < npend && ordered_cas_held<C>(cas_old, li);
 #elif BC_ORD_CAS
             const bool win =
@@ -801,14 +765,7 @@ __global__ void __launch_bounds__(BC_ORD_NT, BC_ORD_MINB) ordered512_kernel(
             const bool win = valid && t < npend && ordered_check(p, own_cur, slot_shift, x, li);
 #endif
             const bool lose = valid && !win;
-#if BC_ORD_TAG
-            // out of range of this round's base: stay pending without a claim
-            // (the next base is the oldest pending index, so range returns)
-            if (lose && li - base_cur < kRelLimit)
-                ordered_claim_tag<C>(p, own_nxt, slot_shift, x, tag_cur | (li - base_cur));
-#else
             if (lose) ordered_claim(p, own_nxt, slot_shift, x, li);
-#endif
 #if BC_ORD_PF & 2
             if (valid && t >= npend) ordered_prefetch<C>(p, words, x);  // checked next round
 #endif
@@ -818,12 +775,6 @@ __global__ void __launch_bounds__(BC_ORD_NT, BC_ORD_MINB) ordered512_kernel(
             t_chk += tb_ - ta;
 #endif
             u32 base = 0;
-#if BC_ORD_TAG
-            if (lm) {
-                const u32 mn = __reduce_min_sync(kFull, lose ? li : kUnclaimed);
-                if (lane == 0) atomicMin(&s_min, mn);
-            }
-#endif
             if (lm && lane == 0) base = atomicAdd(&s_cnt, (u32)__popc(lm));
 #if BC_ORD_DYN
             const u32 t1 = next_tile();
@@ -833,13 +784,7 @@ __global__ void __launch_bounds__(BC_ORD_NT, BC_ORD_MINB) ordered512_kernel(
             u32 li_n = 0;
             u64 x_n = 0;
             const bool valid_n = fetch(t1 + lane, li_n, x_n);
-#if BC_ORD_TAG
-            // the next tile's claim loads are in flight during this tile's commit
-            u32 cas_n[C];
-            const u32 rel_n = li_n - base_prev;
-            ordered_tag_issue<C>(p, own_cur, slot_shift, x_n,
-                                 valid_n && t1 + lane < npend && rel_n < kRelLimit, cas_n);
-#elif BC_ORD_PIPE
+#if BC_ORD_PIPE
             // the next tile's checks are in flight during this tile's commit
             u32 cas_n[C];
             ordered_cas_issue<C>(p, own_cur, slot_shift, x_n, li_n, valid_n && t1 + lane < npend,
@@ -876,10 +821,7 @@ __global__ void __launch_bounds__(BC_ORD_NT, BC_ORD_MINB) ordered512_kernel(
             li = li_n;
             x = x_n;
             valid = valid_n;
-#if BC_ORD_TAG
-            rel = rel_n;
-#endif
-#if BC_ORD_PIPE || BC_ORD_TAG
+#if BC_ORD_PIPE
 #pragma unroll
             for (int ci = 0; ci < C; ++ci) cas_old[ci] = cas_n[ci];
 #endif
@@ -891,9 +833,6 @@ __global__ void __launch_bounds__(BC_ORD_NT, BC_ORD_MINB) ordered512_kernel(
         __syncthreads();  // the round's local appends are complete
         if (threadIdx.x == 0) {
             s_pend = s_cnt;
-#if BC_ORD_TAG
-            if (s_cnt) atomicMin(state + 8u + round % 3u, s_min);
-#endif
             if (s_cnt) atomicAdd(state + round % 3u, s_cnt);
             if (s_exh) atomicOr(state + round % 3u, 0x80000000u);
         }
@@ -914,15 +853,6 @@ __global__ void __launch_bounds__(BC_ORD_NT, BC_ORD_MINB) ordered512_kernel(
 #endif
         const u32 rw = __ldcg(state + round % 3u);
         const bool more = (rw & 0x7fffffffu) != 0 || !(rw >> 31);
-#if BC_ORD_TAG
-        {
-            // every key that claims next round is pending now (index >= the
-            // minimum) or enters later (index above every pending one)
-            const u32 mp = __ldcg(state + 8u + round % 3u);
-            base_prev = base_cur;
-            if (mp != kUnclaimed) base_cur = mp;
-        }
-#endif
         u32 *tmp = cur;
         cur = nxt;
         nxt = tmp;
@@ -943,6 +873,204 @@ __global__ void __launch_bounds__(BC_ORD_NT, BC_ORD_MINB) ordered512_kernel(
                blockIdx.x, round, ntiles, ncom, t_work / max(round, 1u), t_sync / max(round, 1u),
                t_chk / max(ntiles, 1u), t_rest / max(ntiles, 1u), t_com / max(ncom, 1u));
 #endif
+}
+
+
+// One claim array, one grid sync per round, and a key claims and commits in
+// the same round (BC_ORDERED_ONE, the default for the tiled path):
+//
+//   phase A  every key the CTA holds -- last round's losers and the next
+//            slice of the stream -- claims its candidate slots:
+//            atomicMin(slot, tag_r | li - base_r);
+//   grid sync
+//   phase B  every such key loads its slots; it holds a slot that still shows
+//            its own value.  Holders of all their slots commit (a warp tile at
+//            a time, as in ordered512_kernel), the others go to the next list.
+//
+// There is no sync between phase B and the next round's phase A, so a fast
+// CTA's round r+1 claims (smaller tag) may overwrite a slot before a slow
+// CTA's key has checked it in round r.  That key then sees a foreign value
+// and waits one more round: a false loss, never a false win -- a key wins
+// only where its own round-r value survived, i.e. no earlier key claimed the
+// slot in round r, and every uncommitted earlier key did claim (keys enter in
+// index order, slices of different rounds being separated by a sync).  The
+// commits of round r and the block loads of round r+1 are separated by
+// round r+1's sync.
+//
+// Against ordered512_kernel's two reset-on-win arrays this halves the claim
+// footprint in the L2 (what the rounds are most sensitive to), replaces the
+// c atomicCAS checks of a key by c loads, and commits a window's keys per
+// sync instead of half a window's.
+//
+// Rotating state words (written in phase B of round r, complete at round
+// r+1's sync, read in phase B of round r+1, re-armed in phase B of round r+2):
+// [r % 3] pending total | exhausted << 31, [8 + r % 3] the minimum of the
+// losers' indices and the CTAs' slice ends -- a lower bound of every index
+// that claims from round r+1 on, used as the claim base two rounds later.
+// A key further than 2^24 - 2 above the base skips its claim and waits.
+template <int C, class Src>
+__global__ void __launch_bounds__(BC_ORD_NT, BC_ORD_MINB) ordered1_kernel(
+    const __grid_constant__ KParams p, u64 *__restrict__ words, const Src src, u64 n, u32 cap,
+    u32 *__restrict__ owner, u64 slots, u32 slot_shift, u32 *__restrict__ state,
+    unsigned long long *__restrict__ admitted) {
+    cg::grid_group grid = cg::this_grid();
+    __shared__ WarpSmem<C> smem[BC_ORD_NT / 32];
+    __shared__ u32 s_cnt, s_pend, s_adm, s_exh, s_tile, s_min, s_new;
+    __shared__ u64 s_start;
+    extern __shared__ __align__(16) unsigned char dsm[];
+    WarpSmem<C> &ws = smem[threadIdx.x >> 5];
+    const int lane = threadIdx.x & 31;
+    const u32 wid = threadIdx.x >> 5;
+    u64 *curk = reinterpret_cast<u64 *>(dsm), *nxtk = curk + cap;
+    u32 *cur = reinterpret_cast<u32 *>(nxtk + cap), *nxt = cur + cap;
+    unsigned long long *cursor = reinterpret_cast<unsigned long long *>(state + 4);
+    if (threadIdx.x == 0) s_pend = 0;
+    u32 round = 0, n_admitted = 0;
+    u32 base = 0, base_next = 0;
+    for (;;) {
+        if ((round & 255u) == 0) {
+            // the tag restarts: what the array holds (checked until the end of
+            // the last round, or left by an earlier launch) would outrank it
+            if (round) grid.sync();
+            for (u64 i = blockIdx.x * (u64)BC_ORD_NT + threadIdx.x; i < slots;
+                 i += (u64)gridDim.x * BC_ORD_NT)
+                __stcg(owner + i, kUnclaimed);
+            grid.sync();
+        }
+        const u32 tag = claim_tag(round);
+        if (threadIdx.x == 0) {
+            const u32 free = cap - s_pend;
+            const u64 st = free ? atomicAdd(cursor, (unsigned long long)free) : 0ull;
+            s_start = st;
+            s_adm = (free && st < n) ? (u32)min((u64)free, n - st) : 0u;
+            s_exh = free && st + free >= n;
+            s_cnt = 0;
+            s_new = 0;
+            s_min = kUnclaimed;
+            s_tile = BC_ORD_NT;
+        }
+        __syncthreads();
+        const u32 npend = s_pend, adm = s_adm;
+        const u64 start = s_start;
+        // ---- phase A: claims ----
+        for (u32 t = threadIdx.x; t < npend; t += BC_ORD_NT) {
+            const u32 rel = cur[t] - base;
+            if (rel < kRelLimit) ordered_claim_tag<C>(p, owner, slot_shift, curk[t], tag | rel);
+        }
+        for (u32 t0 = wid * 32; t0 < adm; t0 += BC_ORD_NT) {  // warp-uniform
+            const u32 t = t0 + lane;
+            const u64 idx = start + t;
+            u64 x = 0;
+            const bool ok = t < adm && src.admit(idx, x);
+            const u32 om = __ballot_sync(kFull, ok);
+            u32 at = 0;
+            if (lane == 0 && om) at = atomicAdd(&s_new, (u32)__popc(om));
+            at = __shfl_sync(kFull, at, 0);
+            if (ok) {
+                const u32 slot = npend + at + __popc(om & ((1u << lane) - 1u));
+                cur[slot] = (u32)idx;
+                curk[slot] = x;
+                const u32 rel = (u32)idx - base;
+                if (rel < kRelLimit) ordered_claim_tag<C>(p, owner, slot_shift, x, tag | rel);
+                ++n_admitted;
+            }
+        }
+        __syncthreads();
+        const u32 total = npend + s_new;
+        grid.sync();
+        // ---- last round's outcome ----
+        if (round) {
+            const u32 rw = __ldcg(state + (round - 1u) % 3u);
+            if ((rw & 0x7fffffffu) == 0 && (rw >> 31)) break;  // nothing pending, stream ended
+            const u32 mp = __ldcg(state + 8u + (round - 1u) % 3u);
+            base_next = mp != kUnclaimed ? mp : base;
+        }
+        if (blockIdx.x == 0 && threadIdx.x == 0) {  // round r-2's words: read in round r-1
+            state[(round + 1u) % 3u] = 0;
+            state[8u + (round + 1u) % 3u] = kUnclaimed;
+        }
+        // ---- phase B: checks and commits ----
+        auto fetch = [&](u32 t, u32 &li, u64 &x) -> bool {
+            if (t >= total) return false;
+            li = cur[t];
+            x = curk[t];
+            return true;
+        };
+        auto next_tile = [&]() -> u32 {
+            u32 v = 0;
+            if (lane == 0) v = atomicAdd(&s_tile, 32u);
+            return __shfl_sync(kFull, v, 0);
+        };
+        u32 t0 = wid * 32;
+        u32 li = 0;
+        u64 x = 0;
+        bool valid = fetch(t0 + lane, li, x);
+        u32 rel = li - base;
+        u32 seen[C];
+        ordered_tag_issue<C>(p, owner, slot_shift, x, valid && rel < kRelLimit, seen);
+        while (t0 < total) {
+            const bool win = valid && rel < kRelLimit && ordered_cas_held<C>(seen, tag | rel);
+            const bool lose = valid && !win;
+            const u32 lm = __ballot_sync(kFull, lose);
+            u32 at = 0;
+            if (lm) {
+                const u32 mn = __reduce_min_sync(kFull, lose ? li : kUnclaimed);
+                if (lane == 0) {
+                    atomicMin(&s_min, mn);
+                    at = atomicAdd(&s_cnt, (u32)__popc(lm));
+                }
+            }
+            const u32 t1 = next_tile();
+            u32 li_n = 0;
+            u64 x_n = 0;
+            const bool valid_n = fetch(t1 + lane, li_n, x_n);
+            const u32 rel_n = li_n - base;
+            u32 seen_n[C];  // the next tile's claim loads fly during this tile's commit
+            ordered_tag_issue<C>(p, owner, slot_shift, x_n, valid_n && rel_n < kRelLimit, seen_n);
+            if (__ballot_sync(kFull, win)) {
+                phase1<C, true>(p, x, win, ws, lane);
+                __syncwarp();
+                phase2<OP_INSERT, C, BC_ORD_UNR>(p, words, ws, lane);
+                __syncwarp();
+            }
+            if (lm) {
+                at = __shfl_sync(kFull, at, 0);
+                if (lose) {
+                    const u32 slot = at + __popc(lm & ((1u << lane) - 1u));
+                    nxt[slot] = li;
+                    nxtk[slot] = x;
+                }
+            }
+            li = li_n;
+            x = x_n;
+            valid = valid_n;
+            rel = rel_n;
+#pragma unroll
+            for (int ci = 0; ci < C; ++ci) seen[ci] = seen_n[ci];
+            t0 = t1;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            s_pend = s_cnt;
+            u32 m = s_min;
+            if (adm) m = min(m, (u32)(start + adm));  // bounds every later slice from below
+            if (m != kUnclaimed) atomicMin(state + 8u + round % 3u, m);
+            if (s_cnt) atomicAdd(state + round % 3u, s_cnt);
+            if (s_exh) atomicOr(state + round % 3u, 0x80000000u);
+        }
+        u32 *tmp = cur;
+        cur = nxt;
+        nxt = tmp;
+        u64 *tmpk = curk;
+        curk = nxtk;
+        nxtk = tmpk;
+        base = base_next;
+        ++round;
+    }
+    if (Src::kCounts && admitted != nullptr) {
+        for (int o = 16; o > 0; o >>= 1) n_admitted += __shfl_xor_sync(kFull, n_admitted, o);
+        if (lane == 0 && n_admitted) atomicAdd(admitted, (unsigned long long)n_admitted);
+    }
 }
 
 template <int OP>
@@ -1342,6 +1470,28 @@ static const void *ordered512_ptr(u32 c) {
     }
 }
 
+// BC_ORDERED_ONE=0: the two-array reset-on-win rounds (ordered512_kernel)
+bool ordered_one() {
+    static const bool on = [] {
+        const char *e = getenv("BC_ORDERED_ONE");
+        return e == nullptr || atoi(e) != 0;
+    }();
+    return on;
+}
+
+template <class Src>
+static const void *ordered1_ptr(u32 c) {
+    switch (c) {
+        case 2: return (const void *)ordered1_kernel<2, Src>;
+        case 3: return (const void *)ordered1_kernel<3, Src>;
+        case 4: return (const void *)ordered1_kernel<4, Src>;
+        case 5: return (const void *)ordered1_kernel<5, Src>;
+        case 6: return (const void *)ordered1_kernel<6, Src>;
+        case 7: return (const void *)ordered1_kernel<7, Src>;
+        default: return (const void *)ordered1_kernel<8, Src>;
+    }
+}
+
 u64 ordered_owner_words(u64 num_blocks, u64 slots) {
     // window kernel: two arrays of `slots` u32 claims; fixed-chunk kernel:
     // one array of num_blocks u64 round-tagged claims
@@ -1365,7 +1515,10 @@ static cudaError_t launch_window(const KParams &p, u64 *words, const Src *src, c
     cudaError_t e = cudaMemsetAsync(state + 1, 0, 3 * sizeof(u32), s);
     if (e != cudaSuccess) return e;
     const bool tile = src != nullptr;
-    const void *fw = tile ? ordered512_ptr<Src>(p.c) : (const void *)ordered_window_kernel;
+    const bool one = tile && ordered_one();
+    const void *fw = one    ? ordered1_ptr<Src>(p.c)
+                     : tile ? ordered512_ptr<Src>(p.c)
+                            : (const void *)ordered_window_kernel;
     const unsigned grid = grid_for(fw, 256, 0, (chunk + 255) / 256);
     u32 slot_shift = 0;  // identity slots when there is one per block
     if (slots < p.num_blocks) slot_shift = 64u - (u32)__builtin_ctzll(slots);
@@ -1380,7 +1533,7 @@ static cudaError_t launch_window(const KParams &p, u64 *words, const Src *src, c
     cfg.numAttrs = 1;
     size_t bytes = 0;
     float hit = 0.f;
-    const size_t claim_bytes = sizeof(u32) * 2 * slots;
+    const size_t claim_bytes = sizeof(u32) * (one ? 1 : 2) * slots;
     // The set-aside is sized to the claims, not to the device maximum: what
     // it takes beyond them is lost to the candidate blocks and the dirty
     // lines of the commits (B200: cfg3 5 395 -> 6 140 Mkeys/s, cfg5 with 2^22
@@ -1441,6 +1594,9 @@ static cudaError_t launch_window(const KParams &p, u64 *words, const Src *src, c
     switch (p.c) {
 #define BC_ORD_C(c)                                                                         \
     case c:                                                                                 \
+        if (one)                                                                            \
+            return cudaLaunchKernelEx(&cfg, ordered1_kernel<c, Src>, p, words, *src, n,     \
+                                      cap, own, slots, slot_shift, state, admitted);        \
         return cudaLaunchKernelEx(&cfg, ordered512_kernel<c, Src>, p, words, *src, n, cap,   \
                                   own, slots, slot_shift, state, admitted);
         BC_ORD_C(2) BC_ORD_C(3) BC_ORD_C(4) BC_ORD_C(5) BC_ORD_C(6) BC_ORD_C(7) BC_ORD_C(8)

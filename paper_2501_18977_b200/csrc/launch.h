@@ -42,6 +42,7 @@ cudaError_t launch_relaxed_peers(const KParams &p, u64 *const *parts, int nparts
 // lists: 2 * chunk u32 stream indices; lkeys: 2 * chunk u64 keys (the
 // pending lists of the tiled kernel).  chunk == 0 is rejected.
 bool ordered_window_mode();
+bool ordered_one();  // one claim array, same-round commits (ordered1_kernel)
 bool ordered_tiles_supported(const KParams &p);
 u64 ordered_owner_words(u64 num_blocks, u64 slots);
 cudaError_t launch_ordered(const KParams &p, u64 *words, const u64 *keys, u64 n, u64 chunk,

@@ -435,7 +435,10 @@ static u64 ticket_chunk() { return std::max<u64>(1, env_u64("BC_TICKET_CHUNK", 1
 bool ordered_ticket_supported(const KParams &p) {
     if (!(p.fast_random && p.wpb == 8 && p.c >= 2 && p.c <= 8)) return false;
     if (env_u64("BC_ORDERED_TICKET", 1) == 0) return false;
-    const u64 dflt = p.c >= 3 ? (1ull << 21) : (1ull << 20);
+    // crossover with the one-array claim rounds (tools/r2_crossover.sh, Mkeys/s
+    // ticket / claims): c = 2, 2^19 blocks 4 002 / 3 367, 2^20 4 143 / 4 302;
+    // c = 3, 2^20 blocks 2 222 / 1 566, 2^21 2 471 / 2 766
+    const u64 dflt = p.c >= 3 ? (3ull << 19) : (3ull << 18);
     return p.num_blocks <= env_u64("BC_TICKET_MAX_BLOCKS", dflt);
 }
 

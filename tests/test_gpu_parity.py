@@ -206,14 +206,18 @@ def test_cfg3_properties_full_size():
     ("cfg3", 3, 16, 16 * 2**28, 2**23),
     # config 5 geometry: 8 GiB, M = 2^27 blocks hashed onto 2^23 claim slots
     ("cfg5", 2, 11, 2**36, 2**22),
-    # the ticket dataflow's largest defaults: 2^20 blocks (c = 2), 2^21 (c = 3)
-    ("ticket_2p20", 2, 14, 2**29, 2**23),
-    ("ticket_2p21_c3", 3, 16, 2**30, 2**23),
+    # the ticket dataflow's largest defaults: 3 * 2^18 blocks (c = 2), 3 * 2^19 (c = 3)
+    ("ticket_max_c2", 2, 14, 3 * 2**27, 2**23),
+    ("ticket_max_c3", 3, 16, 3 * 2**28, 2**23),
+    # the smallest filters on the claim rounds: identity claim slots, window M / 2
+    ("claims_2p20", 2, 14, 2**29, 2**23),
+    ("claims_2p21_c3", 3, 16, 2**30, 2**23),
 ])
 def test_exact_order_full_geometry_matches_oracle(name, c, k, size_bits, n):
     """Exact-order builds on the full-size filters of configs 3 and 5 (claim
-    rounds) and at the ticket dataflow's largest default sizes (only the key
-    count is reduced so the sequential oracle finishes in seconds):
+    rounds), at the ticket dataflow's largest default sizes and just above
+    them (only the key count is reduced so the sequential oracle finishes in
+    seconds):
     bit-identical words, and identical answers on a mixed probe set."""
     cfg = bb.FilterConfig(kind="blowchoc", k=k, choices=c, size_bits=size_bits, seed=1)
     keys = bb.even_keys(n, 11)
