@@ -908,8 +908,13 @@ __global__ void __launch_bounds__(BC_ORD_NT, BC_ORD_MINB) ordered512_kernel(
 // losers' indices and the CTAs' slice ends -- a lower bound of every index
 // that claims from round r+1 on, used as the claim base two rounds later.
 // A key further than 2^24 - 2 above the base skips its claim and waits.
+#ifndef BC_ORD1_MINB2
+#define BC_ORD1_MINB2 2  // c = 2: 2 CTAs per SM at <= 128 registers (cfg5 9 112 -> 9 497 Mkeys/s, cfg4's geometry equal)
+#endif
+constexpr int ord1_minb(int C) { return C == 2 ? BC_ORD1_MINB2 : BC_ORD_MINB; }
+
 template <int C, class Src>
-__global__ void __launch_bounds__(BC_ORD_NT, BC_ORD_MINB) ordered1_kernel(
+__global__ void __launch_bounds__(BC_ORD_NT, ord1_minb(C)) ordered1_kernel(
     const __grid_constant__ KParams p, u64 *__restrict__ words, const Src src, u64 n, u32 cap,
     u32 *__restrict__ owner, u64 slots, u32 slot_shift, u32 *__restrict__ state,
     unsigned long long *__restrict__ admitted) {
@@ -927,6 +932,10 @@ __global__ void __launch_bounds__(BC_ORD_NT, BC_ORD_MINB) ordered1_kernel(
     if (threadIdx.x == 0) s_pend = 0;
     u32 round = 0, n_admitted = 0;
     u32 base = 0, base_next = 0;
+#ifdef BC_ORD_PROF
+    long long t_a = 0, t_sync = 0, t_b = 0, tq = clock64();
+    u32 n_lost = 0, n_seen = 0;
+#endif
     for (;;) {
         if ((round & 255u) == 0) {
             // the tag restarts: what the array holds (checked until the end of
@@ -977,7 +986,21 @@ __global__ void __launch_bounds__(BC_ORD_NT, BC_ORD_MINB) ordered1_kernel(
         }
         __syncthreads();
         const u32 total = npend + s_new;
+#ifdef BC_ORD_PROF
+        {
+            const long long t_ = clock64();
+            t_a += t_ - tq;
+            tq = t_;
+        }
+#endif
         grid.sync();
+#ifdef BC_ORD_PROF
+        {
+            const long long t_ = clock64();
+            t_sync += t_ - tq;
+            tq = t_;
+        }
+#endif
         // ---- last round's outcome ----
         if (round) {
             const u32 rw = __ldcg(state + (round - 1u) % 3u);
@@ -1012,6 +1035,10 @@ __global__ void __launch_bounds__(BC_ORD_NT, BC_ORD_MINB) ordered1_kernel(
             const bool win = valid && rel < kRelLimit && ordered_cas_held<C>(seen, tag | rel);
             const bool lose = valid && !win;
             const u32 lm = __ballot_sync(kFull, lose);
+#ifdef BC_ORD_PROF
+            n_lost += __popc(lm);
+            n_seen += __popc(__ballot_sync(kFull, valid));
+#endif
             u32 at = 0;
             if (lm) {
                 const u32 mn = __reduce_min_sync(kFull, lose ? li : kUnclaimed);
@@ -1066,7 +1093,21 @@ __global__ void __launch_bounds__(BC_ORD_NT, BC_ORD_MINB) ordered1_kernel(
         nxtk = tmpk;
         base = base_next;
         ++round;
+#ifdef BC_ORD_PROF
+        {
+            const long long t_ = clock64();
+            t_b += t_ - tq;
+            tq = t_;
+        }
+#endif
     }
+#ifdef BC_ORD_PROF
+    if (lane == 0 && (blockIdx.x % 64) == 0 && wid == 0)
+        printf("ord1 prof cta %u rounds %u per round: claims %lld sync %lld commits %lld; warp 0 saw %u "
+               "keys, %u lost\n",
+               blockIdx.x, round, t_a / max(round, 1u), t_sync / max(round, 1u),
+               t_b / max(round, 1u), n_seen, n_lost);
+#endif
     if (Src::kCounts && admitted != nullptr) {
         for (int o = 16; o > 0; o >>= 1) n_admitted += __shfl_xor_sync(kFull, n_admitted, o);
         if (lane == 0 && n_admitted) atomicAdd(admitted, (unsigned long long)n_admitted);
@@ -1569,7 +1610,8 @@ static cudaError_t launch_window(const KParams &p, u64 *words, const Src *src, c
     if (e == cudaSuccess) e = cudaMemsetAsync(state + 8, 0xff, 8 * sizeof(u32), s);  // minima
     if (e != cudaSuccess) return e;
     const int sms = (int)sm_count();
-    u64 ctas = std::max<u64>(1, std::min<u64>((u64)sms * BC_ORD_MINB, chunk / BC_ORD_NT));
+    const int minb = one ? ord1_minb((int)p.c) : BC_ORD_MINB;
+    u64 ctas = std::max<u64>(1, std::min<u64>((u64)sms * minb, chunk / BC_ORD_NT));
     u32 cap = 0;
     size_t smem = 0;
     for (int it = 0;; ++it) {
