@@ -8,11 +8,15 @@
 //                            tile's hashing overlapped with the loads
 //   lookup512_kernel<C, K>   lookups: staged blocks, early exit over choices
 //   lookup512_pipe_kernel<K> single-choice lookups, two tiles in flight
-//   ordered512_kernel<C,Src> exact stream-order insert for c >= 2, 512-bit
+//   ordered1_kernel<C,Src>   exact stream-order insert for c >= 2, 512-bit
 //                            blocks: claim rounds over a sliding window, one
-//                            cooperative launch, winners committed a warp
-//                            tile at a time; keys from an array or encoded
-//                            from a DNA sequence on the fly (keysrc.cuh)
+//                            cooperative launch, one array of epoch-tagged
+//                            claims, one grid sync per round, winners
+//                            committed a warp tile at a time; keys from an
+//                            array or encoded from a DNA sequence on the fly
+//                            (keysrc.cuh)
+//   ordered512_kernel<C,Src> its predecessor (BC_ORDERED_ONE=0): two claim
+//                            arrays, claims reset by the winners' atomicCAS
 //   ordered_window_kernel    the same rounds for any geometry, thread-per-key
 //                            commits (ordered_kernel: fixed-chunk variant)
 //   flat_kernel<OP>          standard Bloom filter (k global bits)
@@ -1279,7 +1283,7 @@ static bool l2_window(size_t fbytes, size_t *bytes, float *hit_ratio, bool fit =
     }
     size_t limit = fit ? std::min(i->persist, (fbytes + (1u << 20) - 1) & ~(size_t)((1u << 20) - 1))
                        : i->persist;
-    if (cap) limit = std::min(limit, cap);
+    if (cap) limit = std::min(i->persist, cap);  // explicit size (experiments)
     if (!i->on || i->limit != limit) {
         if (cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, limit) != cudaSuccess) {
             cudaGetLastError();

@@ -9,7 +9,7 @@ python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; echo "sm
 for c in 5 1 2 3 4; do
   timeout 1500 python bench.py --config $c > $O/bench_cfg$c.json 2> $O/bench_cfg$c.err; echo "cfg$c rc=$?"
 done
-for c in 1 3 5; do
+for c in 1 3 4 5; do
   timeout 1500 python bench.py --config $c --insert-mode ordered --no-cpu-baseline > $O/bench_cfg${c}_ordered.json 2> $O/bo$c.err; echo "cfg$c ordered rc=$?"
 done
 timeout 900 python bench.py --impl reference > $O/bench_reference_cfg5.json 2> $O/ref.err; echo "ref rc=$?"
