@@ -525,10 +525,11 @@ __device__ __forceinline__ bool ordered_cas_held(const u32 (&old)[C], u32 li) {
 // is ever reset: the check is a plain load compared with the key's own value.
 // The array is cleared in-kernel when the 8-bit tag wraps (every 256 rounds)
 // and in a launch's first round.
-constexpr u32 kRelBits = 24;
-constexpr u32 kRelLimit = (1u << kRelBits) - 1u;  // 0xffffffff is never a claim
+constexpr u32 kRelBits = 24;  // default; BC_ORDERED_REL_BITS narrows it (tests of the out-of-range path)
 
-__device__ __forceinline__ u32 claim_tag(u32 round) { return (255u - (round & 255u)) << kRelBits; }
+__device__ __forceinline__ u32 claim_tag(u32 round, u32 rel_bits) {
+    return (255u - (round & 255u)) << rel_bits;
+}
 
 template <int C>
 __device__ __forceinline__ void ordered_tag_issue(const KParams &p, const u32 *own_cur,
@@ -921,8 +922,9 @@ template <int C, class Src>
 __global__ void __launch_bounds__(BC_ORD_NT, ord1_minb(C)) ordered1_kernel(
     const __grid_constant__ KParams p, u64 *__restrict__ words, const Src src, u64 n, u32 cap,
     u32 *__restrict__ owner, u64 slots, u32 slot_shift, u32 *__restrict__ state,
-    unsigned long long *__restrict__ admitted) {
+    unsigned long long *__restrict__ admitted, u32 rel_bits) {
     cg::grid_group grid = cg::this_grid();
+    const u32 kRelLimit = (1u << rel_bits) - 1u;  // 0xffffffff is never a claim
     __shared__ WarpSmem<C> smem[BC_ORD_NT / 32];
     __shared__ u32 s_cnt, s_pend, s_adm, s_exh, s_tile, s_min, s_new;
     __shared__ u64 s_start;
@@ -950,7 +952,7 @@ __global__ void __launch_bounds__(BC_ORD_NT, ord1_minb(C)) ordered1_kernel(
                 __stcg(owner + i, kUnclaimed);
             grid.sync();
         }
-        const u32 tag = claim_tag(round);
+        const u32 tag = claim_tag(round, rel_bits);
         if (threadIdx.x == 0) {
             const u32 free = cap - s_pend;
             const u64 st = free ? atomicAdd(cursor, (unsigned long long)free) : 0ull;
@@ -1636,13 +1638,19 @@ static cudaError_t launch_window(const KParams &p, u64 *words, const Src *src, c
     cfg.gridDim = dim3((unsigned)ctas);
     cfg.blockDim = dim3(BC_ORD_NT);
     cfg.dynamicSmemBytes = smem;
+    static const u32 rel_bits = [] {
+        const char *e = getenv("BC_ORDERED_REL_BITS");
+        const int v = e ? atoi(e) : (int)kRelBits;
+        return (u32)std::min(std::max(v, 1), (int)kRelBits);
+    }();
     count_launch();
     switch (p.c) {
 #define BC_ORD_C(c)                                                                         \
     case c:                                                                                 \
         if (one)                                                                            \
             return cudaLaunchKernelEx(&cfg, ordered1_kernel<c, Src>, p, words, *src, n,     \
-                                      cap, own, slots, slot_shift, state, admitted);        \
+                                      cap, own, slots, slot_shift, state, admitted,         \
+                                      rel_bits);                                            \
         return cudaLaunchKernelEx(&cfg, ordered512_kernel<c, Src>, p, words, *src, n, cap,   \
                                   own, slots, slot_shift, state, admitted);
         BC_ORD_C(2) BC_ORD_C(3) BC_ORD_C(4) BC_ORD_C(5) BC_ORD_C(6) BC_ORD_C(7) BC_ORD_C(8)

@@ -668,11 +668,16 @@ def test_extreme_keys(kind, c, strategy, bb_bits):
     assert f.contains_many(keys[::2]).all()
 
 
+@pytest.mark.parametrize("one", ["1", "0"])
 @pytest.mark.parametrize("slots", ["64", "4096"])
-def test_ordered_build_with_hashed_claim_slots(golden, slots):
+def test_ordered_build_with_hashed_claim_slots(golden, slots, one):
     """Exact-order inserts with the claim tags hashed onto few slots
     (BC_ORDERED_SLOTS, read when the scratch is allocated): spurious
-    conflicts only delay commits, the bits stay the reference's."""
+    conflicts only delay commits, the bits stay the reference's.  With 64
+    slots the build takes hundreds of rounds, so the one-array kernel's 8-bit
+    round tag wraps (the in-kernel clear of the claims).  Both claim-round
+    kernels: one array of epoch-tagged claims (default) and two reset-on-win
+    arrays (BC_ORDERED_ONE=0)."""
     meta, _ = golden
     case = meta["bc3_k12_20k"]
     script = (
@@ -682,8 +687,8 @@ def test_ordered_build_with_hashed_claim_slots(golden, slots):
         f"keys = bb.even_keys({case['n_insert']}, {case['insert_seed']})\n"
         "f.insert_many(keys[:7000]); f.insert_many(keys[7000:])\n"
         "print(hashlib.sha256(f.storage.words.tobytes()).hexdigest())\n")
-    assert _run_with_env(script, BC_ORDERED_SLOTS=slots, BC_ORDERED_TICKET="0") == \
-        case["words_sha256"]
+    assert _run_with_env(script, BC_ORDERED_SLOTS=slots, BC_ORDERED_TICKET="0",
+                         BC_ORDERED_ONE=one) == case["words_sha256"]
 
 
 GRID = {"BC_ORDERED_TICKET": "0"}  # exact inserts on the grid-wide claim rounds
@@ -695,6 +700,12 @@ GRID = {"BC_ORDERED_TICKET": "0"}  # exact inserts on the grid-wide claim rounds
                                       ("bc3_k12_20k", {**GRID, "BC_ORDERED_TILES": "0"}),
                                       ("cfg1", {**GRID, "BC_ORDERED_TILES": "0"}),
                                       ("cfg1", GRID), ("bc3_k12_20k", GRID),
+                                      ("cfg1", {**GRID, "BC_ORDERED_ONE": "0"}),
+                                      ("bc3_k12_20k", {**GRID, "BC_ORDERED_ONE": "0"}),
+                                      ("cfg3_small", {**GRID, "BC_ORDERED_ONE": "0"}),
+                                      ("cfg1", {**GRID, "BC_ORDERED_REL_BITS": "10"}),
+                                      ("cfg3_small", {**GRID, "BC_ORDERED_REL_BITS": "6"}),
+                                      ("bc2_k6_t4", {**GRID, "BC_ORDERED_REL_BITS": "3"}),
                                       ("bc4_k8", GRID), ("cfg3_small", GRID),
                                       ("bc8_k5", GRID), ("bc2_k6_t4", GRID),
                                       ("cfg1", {"BC_TICKET_INFLIGHT_PCT": "3"}),
@@ -705,7 +716,10 @@ GRID = {"BC_ORDERED_TICKET": "0"}  # exact inserts on the grid-wide claim rounds
 def test_fallback_kernels_match_reference(golden, name, env):
     """The kernel variants kept behind switches (unpipelined single-choice
     lookups, the grid-wide exact inserts that small filters no longer use,
-    fixed-chunk exact inserts, exact inserts that commit one thread per key)
+    the two-array claim rounds, the one-array rounds with a claim range of a
+    few keys only (BC_ORDERED_REL_BITS: most keys are out of range of the
+    round's base and wait without a claim), fixed-chunk exact inserts, exact
+    inserts that commit one thread per key)
     and the ticket exact insert with narrow / wide in-flight windows and
     several ticket sets per call still give the reference's bits and
     answers."""
@@ -870,7 +884,9 @@ def test_concurrent_lookups_from_threads(golden):
     assert sum(counts) == case["hits_pos"] + case["hits_neg"]
 
 
-@pytest.mark.parametrize("env", [{"BC_TICKET_CHUNK": "1000"}, {"BC_ORDERED_TICKET": "0"}])
+@pytest.mark.parametrize("env", [{"BC_TICKET_CHUNK": "1000"}, {"BC_ORDERED_TICKET": "0"},
+                                 {"BC_ORDERED_TICKET": "0", "BC_ORDERED_ONE": "0"},
+                                 {"BC_ORDERED_TICKET": "0", "BC_ORDERED_REL_BITS": "7"}])
 def test_fused_exact_qgram_insert_in_ticket_sets_and_claim_rounds(env):
     """The fused exact-order q-gram insert of a reads matrix (fixed-length
     records) split into many ticket sets (each set's stream resumes mid-record)
@@ -892,3 +908,29 @@ def test_fused_exact_qgram_insert_in_ticket_sets_and_claim_rounds(env):
         "print(bool(np.array_equal(f.storage.words, o.words)), want.size)\n")
     ok, n = _run_with_env(script, **env).split()
     assert ok == "True" and int(n) > 10000
+
+
+@pytest.mark.parametrize("env", [{}, {"BC_ORDERED_REL_BITS": "10"}, {"BC_ORDERED_ONE": "0"}])
+def test_fused_exact_qgram_insert_across_a_long_invalid_run(env):
+    """A sequence with 300,000 non-ACGT bytes in the middle, inserted by the
+    fused exact-order claim rounds: the stream cursor crosses the run without
+    admitting a key, so the claim base lags far behind the next valid windows
+    (out of claim range when the range is narrowed to 2^10); the words equal
+    the oracle's stream-order insert of encode_qgrams."""
+    script = (
+        "import numpy as np, paper_2501_18977_b200 as bb\n"
+        "from oracle import oracle as orc\n"
+        "rng = np.random.default_rng(5)\n"
+        "a = rng.choice(np.frombuffer(b'ACGT', np.uint8), size=40000)\n"
+        "b = rng.choice(np.frombuffer(b'ACGT', np.uint8), size=50000)\n"
+        "seq = np.concatenate([a, np.full(300000, ord('N'), np.uint8), b]).tobytes()\n"
+        "enc = bb.QGramEncoder(25, canonical=True)\n"
+        "want = orc.encode_qgrams(seq, 25, True)\n"
+        "cfg = dict(kind='blowchoc', k=10, choices=2, n_capacity=want.size, seed=8)\n"
+        "f = bb.Filter.from_config(bb.FilterConfig(**cfg))\n"
+        "assert f.insert_qgrams(enc, seq) == want.size\n"
+        "o = orc.make_filter(**cfg)\n"
+        "o.insert_many(want)\n"
+        "print(bool(np.array_equal(f.storage.words, o.words)), want.size)\n")
+    ok, n = _run_with_env(script, BC_ORDERED_TICKET="0", **env).split()
+    assert ok == "True" and int(n) == 40000 - 24 + 50000 - 24
