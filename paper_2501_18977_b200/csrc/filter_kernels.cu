@@ -926,7 +926,7 @@ __global__ void __launch_bounds__(BC_ORD_NT, ord1_minb(C)) ordered1_kernel(
     cg::grid_group grid = cg::this_grid();
     const u32 kRelLimit = (1u << rel_bits) - 1u;  // 0xffffffff is never a claim
     __shared__ WarpSmem<C> smem[BC_ORD_NT / 32];
-    __shared__ u32 s_cnt, s_pend, s_adm, s_exh, s_tile, s_min, s_new;
+    __shared__ u32 s_cnt, s_adm, s_exh, s_tile, s_min, s_new;
     __shared__ u64 s_start;
     extern __shared__ __align__(16) unsigned char dsm[];
     WarpSmem<C> &ws = smem[threadIdx.x >> 5];
@@ -935,8 +935,8 @@ __global__ void __launch_bounds__(BC_ORD_NT, ord1_minb(C)) ordered1_kernel(
     u64 *curk = reinterpret_cast<u64 *>(dsm), *nxtk = curk + cap;
     u32 *cur = reinterpret_cast<u32 *>(nxtk + cap), *nxt = cur + cap;
     unsigned long long *cursor = reinterpret_cast<unsigned long long *>(state + 4);
-    if (threadIdx.x == 0) s_pend = 0;
     u32 round = 0, n_admitted = 0;
+    u32 npend = 0;  // this CTA's losers of the last round, at the front of cur
     u32 base = 0, base_next = 0;
 #ifdef BC_ORD_PROF
     long long t_a = 0, t_sync = 0, t_b = 0, tq = clock64();
@@ -953,45 +953,57 @@ __global__ void __launch_bounds__(BC_ORD_NT, ord1_minb(C)) ordered1_kernel(
             grid.sync();
         }
         const u32 tag = claim_tag(round, rel_bits);
+        // ---- phase A: claims ----
+        // the slice's round trip to the cursor runs under the losers' claims
         if (threadIdx.x == 0) {
-            const u32 free = cap - s_pend;
+            const u32 free = cap - npend;
             const u64 st = free ? atomicAdd(cursor, (unsigned long long)free) : 0ull;
             s_start = st;
             s_adm = (free && st < n) ? (u32)min((u64)free, n - st) : 0u;
             s_exh = free && st + free >= n;
-            s_cnt = 0;
             s_new = 0;
             s_min = kUnclaimed;
             s_tile = BC_ORD_NT;
         }
-        __syncthreads();
-        const u32 npend = s_pend, adm = s_adm;
-        const u64 start = s_start;
-        // ---- phase A: claims ----
         for (u32 t = threadIdx.x; t < npend; t += BC_ORD_NT) {
             const u32 rel = cur[t] - base;
             if (rel < kRelLimit) ordered_claim_tag<C>(p, owner, slot_shift, curk[t], tag | rel);
         }
-        for (u32 t0 = wid * 32; t0 < adm; t0 += BC_ORD_NT) {  // warp-uniform
-            const u32 t = t0 + lane;
-            const u64 idx = start + t;
-            u64 x = 0;
-            const bool ok = t < adm && src.admit(idx, x);
-            const u32 om = __ballot_sync(kFull, ok);
-            u32 at = 0;
-            if (lane == 0 && om) at = atomicAdd(&s_new, (u32)__popc(om));
-            at = __shfl_sync(kFull, at, 0);
-            if (ok) {
-                const u32 slot = npend + at + __popc(om & ((1u << lane) - 1u));
-                cur[slot] = (u32)idx;
-                curk[slot] = x;
-                const u32 rel = (u32)idx - base;
-                if (rel < kRelLimit) ordered_claim_tag<C>(p, owner, slot_shift, x, tag | rel);
-                ++n_admitted;
+        __syncthreads();
+        const u32 adm = s_adm;
+        const u64 start = s_start;
+        // new keys, four tiles of loads in flight per warp
+        for (u32 t0 = wid * 32; t0 < adm; t0 += 4 * BC_ORD_NT) {  // warp-uniform
+            u64 xs[4];
+            bool oks[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const u32 t = t0 + u * BC_ORD_NT + lane;
+                xs[u] = 0;
+                oks[u] = t < adm && src.admit(start + t, xs[u]);
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const u32 om = __ballot_sync(kFull, oks[u]);
+                if (om == 0) continue;  // warp-uniform
+                u32 at = 0;
+                if (lane == 0) at = atomicAdd(&s_new, (u32)__popc(om));
+                at = __shfl_sync(kFull, at, 0);
+                if (oks[u]) {
+                    const u32 idx = (u32)(start + t0 + u * BC_ORD_NT + lane);
+                    const u32 slot = npend + at + __popc(om & ((1u << lane) - 1u));
+                    cur[slot] = idx;
+                    curk[slot] = xs[u];
+                    const u32 rel = idx - base;
+                    if (rel < kRelLimit)
+                        ordered_claim_tag<C>(p, owner, slot_shift, xs[u], tag | rel);
+                    ++n_admitted;
+                }
             }
         }
         __syncthreads();
         const u32 total = npend + s_new;
+        if (threadIdx.x == 0) s_cnt = 0;  // every thread has read last round's count
 #ifdef BC_ORD_PROF
         {
             const long long t_ = clock64();
@@ -1083,12 +1095,12 @@ __global__ void __launch_bounds__(BC_ORD_NT, ord1_minb(C)) ordered1_kernel(
             t0 = t1;
         }
         __syncthreads();
+        npend = s_cnt;
         if (threadIdx.x == 0) {
-            s_pend = s_cnt;
             u32 m = s_min;
             if (adm) m = min(m, (u32)(start + adm));  // bounds every later slice from below
             if (m != kUnclaimed) atomicMin(state + 8u + round % 3u, m);
-            if (s_cnt) atomicAdd(state + round % 3u, s_cnt);
+            if (npend) atomicAdd(state + round % 3u, npend);
             if (s_exh) atomicOr(state + round % 3u, 0x80000000u);
         }
         u32 *tmp = cur;

@@ -8,6 +8,8 @@ LIB=paper_2501_18977_b200/libbbchoc.so
 KERNELS="_ZN2bc27lookup512_pipe_multi_kernelILi2ELi11EEEvNS_7KParamsEPKmS3_mPhPy
 _ZN2bc27lookup512_pipe_multi_kernelILi3ELi16EEEvNS_7KParamsEPKmS3_mPhPy
 _ZN2bc17relaxed512_kernelILi2EEEvNS_7KParamsEPmPKmm
+_ZN2bc15ordered1_kernelILi3ENS_9ArrayKeysEEEvNS_7KParamsEPmT0_mjPjmjS5_Pyj
+_ZN2bc15ordered1_kernelILi2ENS_9ArrayKeysEEEvNS_7KParamsEPmT0_mjPjmjS5_Pyj
 _ZN2bc17ordered512_kernelILi3ENS_9ArrayKeysEEEvNS_7KParamsEPmT0_mjPjmjS5_Py
 _ZN2bc18ticket_exec_kernelILi2ENS_9ArrayKeysEEEvNS_7KParamsEPmT0_mPKjPjS7_Py
 _ZN2bc16blocks512_kernelILi1ELi1EEEvNS_7KParamsEPmPKmmPhPy"
