@@ -523,8 +523,8 @@ __device__ __forceinline__ bool ordered_cas_held(const u32 (&old)[C], u32 li) {
 // claiming that round.  A newer round's claims are smaller than anything an
 // older round left behind, so atomicMin overwrites stale claims and nothing
 // is ever reset: the check is a plain load compared with the key's own value.
-// The array is cleared in-kernel when the 8-bit tag wraps (every 256 rounds)
-// and in a launch's first round.
+// The array is cleared in-kernel when the 8-bit tag wraps (every 256 rounds,
+// counted across launches).
 constexpr u32 kRelBits = 24;  // default; BC_ORDERED_REL_BITS narrows it (tests of the out-of-range path)
 
 __device__ __forceinline__ u32 claim_tag(u32 round, u32 rel_bits) {
@@ -938,21 +938,26 @@ __global__ void __launch_bounds__(BC_ORD_NT, ord1_minb(C)) ordered1_kernel(
     u32 round = 0, n_admitted = 0;
     u32 npend = 0;  // this CTA's losers of the last round, at the front of cur
     u32 base = 0, base_next = 0;
+    // the tags run on across launches (state[12], zero when the scratch is
+    // allocated): an earlier launch's claims are older rounds' claims, so a
+    // short insert does not pay for a clear of the array
+    const u32 epoch0 = __ldcg(state + 12);
 #ifdef BC_ORD_PROF
     long long t_a = 0, t_sync = 0, t_b = 0, tq = clock64();
     u32 n_lost = 0, n_seen = 0;
 #endif
     for (;;) {
-        if ((round & 255u) == 0) {
+        const u32 epoch = epoch0 + round;
+        if ((epoch & 255u) == 0) {
             // the tag restarts: what the array holds (checked until the end of
-            // the last round, or left by an earlier launch) would outrank it
+            // the last round) would outrank it
             if (round) grid.sync();
             for (u64 i = blockIdx.x * (u64)BC_ORD_NT + threadIdx.x; i < slots;
                  i += (u64)gridDim.x * BC_ORD_NT)
                 __stcg(owner + i, kUnclaimed);
             grid.sync();
         }
-        const u32 tag = claim_tag(round, rel_bits);
+        const u32 tag = claim_tag(epoch, rel_bits);
         // ---- phase A: claims ----
         // the slice's round trip to the cursor runs under the losers' claims
         if (threadIdx.x == 0) {
@@ -1119,6 +1124,7 @@ __global__ void __launch_bounds__(BC_ORD_NT, ord1_minb(C)) ordered1_kernel(
         }
 #endif
     }
+    if (blockIdx.x == 0 && threadIdx.x == 0) state[12] = epoch0 + round + 1u;
 #ifdef BC_ORD_PROF
     if (lane == 0 && (blockIdx.x % 64) == 0 && wid == 0)
         printf("ord1 prof cta %u rounds %u per round: claims %lld sync %lld commits %lld; warp 0 saw %u "
@@ -1625,7 +1631,8 @@ static cudaError_t launch_window(const KParams &p, u64 *words, const Src *src, c
     // the window is spread over as many co-resident CTAs as fit, at least
     // 256 entries per CTA
     e = cudaMemsetAsync(state, 0, 8 * sizeof(u32), s);  // round words, cursor
-    if (e == cudaSuccess) e = cudaMemsetAsync(state + 8, 0xff, 8 * sizeof(u32), s);  // minima
+    if (e == cudaSuccess) e = cudaMemsetAsync(state + 8, 0xff, 4 * sizeof(u32), s);  // minima
+    // state[12], ordered1_kernel's tag epoch, carries over from launch to launch
     if (e != cudaSuccess) return e;
     const int sms = (int)sm_count();
     const int minb = one ? ord1_minb((int)p.c) : BC_ORD_MINB;
