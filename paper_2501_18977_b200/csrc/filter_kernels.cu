@@ -547,13 +547,6 @@ __device__ __forceinline__ void ordered_claim_tag(const KParams &p, u32 *own_nxt
         atomicMin(own_nxt + owner_slot(block_index(p, x, ci), slot_shift), v);
 }
 
-template <int C>
-__device__ __forceinline__ void ordered_prefetch(const KParams &p, const u64 *words, u64 x) {
-#pragma unroll
-    for (int ci = 0; ci < C; ++ci)
-        asm volatile("prefetch.global.L2 [%0];" ::"l"(words + block_index(p, x, ci) * 8));
-}
-
 __device__ __forceinline__ void ordered_claim(const KParams &p, u32 *own_nxt, u32 slot_shift,
                                               u64 x, u32 li) {
     for (u32 ci = 0; ci < p.c; ++ci)
@@ -653,9 +646,6 @@ __global__ void __launch_bounds__(256) ordered_window_kernel(
 #ifndef BC_ORD_SKIP
 #define BC_ORD_SKIP 1  // commit tiles: lanes without a winner read nothing (not block 0)
 #endif
-#ifndef BC_ORD_PF
-#define BC_ORD_PF 0  // L2 prefetch of candidate blocks: 1 with the next tile's checks, 2 at first claim, 3 both
-#endif
 #ifndef BC_ORD_MINB
 #define BC_ORD_MINB 3  // <= 80 registers: 3 CTAs per SM (cfg3 +4%, cfg5 +8% over 2 CTAs at 102)
 #endif
@@ -753,9 +743,6 @@ __global__ void __launch_bounds__(BC_ORD_NT, BC_ORD_MINB) ordered512_kernel(
         u32 cas_old[C];
         ordered_cas_issue<C>(p, own_cur, slot_shift, x, li, valid && t0 + lane < npend, cas_old);
 #endif
-#if BC_ORD_PF & 1
-        if (valid && t0 + lane < npend) ordered_prefetch<C>(p, words, x);
-#endif
         while (t0 < total) {
 #ifdef BC_ORD_PROF
             const long long ta = clock64();
@@ -771,9 +758,6 @@ __global__ void __launch_bounds__(BC_ORD_NT, BC_ORD_MINB) ordered512_kernel(
 #endif
             const bool lose = valid && !win;
             if (lose) ordered_claim(p, own_nxt, slot_shift, x, li);
-#if BC_ORD_PF & 2
-            if (valid && t >= npend) ordered_prefetch<C>(p, words, x);  // checked next round
-#endif
             const u32 lm = __ballot_sync(kFull, lose);
 #ifdef BC_ORD_PROF
             const long long tb_ = clock64();
@@ -794,9 +778,6 @@ __global__ void __launch_bounds__(BC_ORD_NT, BC_ORD_MINB) ordered512_kernel(
             u32 cas_n[C];
             ordered_cas_issue<C>(p, own_cur, slot_shift, x_n, li_n, valid_n && t1 + lane < npend,
                                  cas_n);
-#endif
-#if BC_ORD_PF & 1
-            if (valid_n && t1 + lane < npend) ordered_prefetch<C>(p, words, x_n);
 #endif
 #ifdef BC_ORD_PROF
             const long long tc_ = clock64();
@@ -913,6 +894,20 @@ __global__ void __launch_bounds__(BC_ORD_NT, BC_ORD_MINB) ordered512_kernel(
 // losers' indices and the CTAs' slice ends -- a lower bound of every index
 // that claims from round r+1 on, used as the claim base two rounds later.
 // A key further than 2^24 - 2 above the base skips its claim and waits.
+// -DBC_ORD_CHECK: index checks of ordered1_kernel's lists and claim slots
+// (compute-sanitizer is not available on the pool); a violation traps.
+#ifdef BC_ORD_CHECK
+#define BC_ORD_ASSERT(cond)                                                              \
+    do {                                                                                 \
+        if (!(cond)) {                                                                   \
+            printf("ordered1_kernel check failed: %s (line %d, cta %u thread %u)\n", #cond, \
+                   __LINE__, blockIdx.x, threadIdx.x);                                   \
+            __trap();                                                                    \
+        }                                                                                \
+    } while (0)
+#else
+#define BC_ORD_ASSERT(cond) ((void)0)
+#endif
 #ifndef BC_ORD1_MINB2
 #define BC_ORD1_MINB2 2  // c = 2: 2 CTAs per SM at <= 128 registers (cfg5 9 112 -> 9 497 Mkeys/s, cfg4's geometry equal)
 #endif
@@ -970,8 +965,15 @@ __global__ void __launch_bounds__(BC_ORD_NT, ord1_minb(C)) ordered1_kernel(
             s_min = kUnclaimed;
             s_tile = BC_ORD_NT;
         }
+        BC_ORD_ASSERT(npend <= cap);
         for (u32 t = threadIdx.x; t < npend; t += BC_ORD_NT) {
             const u32 rel = cur[t] - base;
+            BC_ORD_ASSERT(cur[t] >= base && cur[t] < n);
+#ifdef BC_ORD_CHECK
+            for (int ci = 0; ci < C; ++ci)
+                BC_ORD_ASSERT(owner_slot(block_index(p, curk[t], ci), slot_shift) < slots &&
+                              block_index(p, curk[t], ci) < p.num_blocks);
+#endif
             if (rel < kRelLimit) ordered_claim_tag<C>(p, owner, slot_shift, curk[t], tag | rel);
         }
         __syncthreads();
@@ -997,6 +999,7 @@ __global__ void __launch_bounds__(BC_ORD_NT, ord1_minb(C)) ordered1_kernel(
                 if (oks[u]) {
                     const u32 idx = (u32)(start + t0 + u * BC_ORD_NT + lane);
                     const u32 slot = npend + at + __popc(om & ((1u << lane) - 1u));
+                    BC_ORD_ASSERT(slot < cap && idx >= base && (u64)idx < n);
                     cur[slot] = idx;
                     curk[slot] = xs[u];
                     const u32 rel = idx - base;
@@ -1008,6 +1011,7 @@ __global__ void __launch_bounds__(BC_ORD_NT, ord1_minb(C)) ordered1_kernel(
         }
         __syncthreads();
         const u32 total = npend + s_new;
+        BC_ORD_ASSERT(total <= cap && s_new <= adm);
         if (threadIdx.x == 0) s_cnt = 0;  // every thread has read last round's count
 #ifdef BC_ORD_PROF
         {
@@ -1087,6 +1091,7 @@ __global__ void __launch_bounds__(BC_ORD_NT, ord1_minb(C)) ordered1_kernel(
                 at = __shfl_sync(kFull, at, 0);
                 if (lose) {
                     const u32 slot = at + __popc(lm & ((1u << lane) - 1u));
+                    BC_ORD_ASSERT(slot < cap);
                     nxt[slot] = li;
                     nxtk[slot] = x;
                 }
