@@ -306,7 +306,18 @@ static int ensure_ordered_scratch(bc_filter *f, cudaStream_t s) {
     // One-array rounds (ordered1_kernel, tools/r2_one_sweep.sh): cfg3 (c = 3)
     // 7 262 / 7 307 / 6 408 Mkeys/s at 3*2^17 / 2^19 / 3*2^18; cfg5 (c = 2)
     // 8 551 / 8 875 / 9 111.
-    u64 chunk = std::min<u64>(M / 2, (ordered_one() && f->kp.c == 2) ? 3ull << 18 : 1ull << 19);
+    // Below 2^23 blocks the one-array rounds want a window of about
+    // M / (2 c^2): a key loses a round when an earlier key of the window
+    // shares one of its c slots, and with M/2 keys in the window most do
+    // (tools/r2_window_sweep.sh, Mkeys/s at M/2, M/4, M/8, M/16: 2^20 blocks
+    // c = 2: 3 970 / 6 074 / 7 004 / 5 743; c = 3: 1 576 / 2 250 / 2 798 /
+    // 4 246; 2^22 blocks c = 2: 9 584 at M/8, c = 3: 6 454 at M/16).
+    const u64 cc = (u64)f->kp.c * f->kp.c;
+    u64 chunk = ordered_one()
+                    ? std::min<u64>(std::max<u64>(M / (2 * cc), 4096),
+                                    f->kp.c == 2 ? 3ull << 18 : 1ull << 19)
+                    : std::min<u64>(M / 2, 1ull << 19);
+    chunk = std::min<u64>(chunk, std::max<u64>(M / 2, 256));
     if (const char *e = std::getenv("BC_ORDERED_CHUNK")) chunk = std::strtoull(e, nullptr, 10);
     chunk = std::max<u64>(chunk, 256);
     chunk = std::min<u64>(chunk, 1ull << 24);

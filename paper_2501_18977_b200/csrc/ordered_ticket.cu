@@ -435,10 +435,12 @@ static u64 ticket_chunk() { return std::max<u64>(1, env_u64("BC_TICKET_CHUNK", 1
 bool ordered_ticket_supported(const KParams &p) {
     if (!(p.fast_random && p.wpb == 8 && p.c >= 2 && p.c <= 8)) return false;
     if (env_u64("BC_ORDERED_TICKET", 1) == 0) return false;
-    // crossover with the one-array claim rounds (tools/r2_crossover.sh, Mkeys/s
-    // ticket / claims): c = 2, 2^19 blocks 4 002 / 3 367, 2^20 4 143 / 4 302;
-    // c = 3, 2^20 blocks 2 222 / 1 566, 2^21 2 471 / 2 766
-    const u64 dflt = p.c >= 3 ? (3ull << 19) : (3ull << 18);
+    // crossover with the one-array claim rounds at their M / (2 c^2) window
+    // (tools/r2_crossover.sh, r2_crossover2.sh; Mkeys/s ticket / claims):
+    // c = 2: 2^18 blocks 3 812 / 3 167, 3*2^17 4 078 / 4 013, 2^19 4 007 / 4 921;
+    // c = 3: 3*2^17 2 242 / 1 431, 2^19 ~1 850 (erratic: 290 .. 1 850) / 2 000,
+    // 3*2^18 2 152 / 2 575
+    const u64 dflt = p.c >= 3 ? (1ull << 19) - 1 : (3ull << 17);
     return p.num_blocks <= env_u64("BC_TICKET_MAX_BLOCKS", dflt);
 }
 

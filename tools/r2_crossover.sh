@@ -6,15 +6,13 @@ import json,sys
 for l in sys.stdin:
     try: d=json.loads(l); print('$c', '$lab', d['ms_median'], d['mkeys_s'], d['bits_equal_reference'])
     except Exception: print(l.strip())"; }
-for lg in 16 17 18 19 20; do
+for lg in 15 16 17 18 19 20; do
   bits=$((512 << lg)); n=$((bits / 16))
   run $bits:$n:2:14 "ticket" A=1
   run $bits:$n:2:14 "claims" BC_ORDERED_TICKET=0
 done
-for lg in 17 19 20 21; do
+for lg in 15 17 18 19 20 21; do
   bits=$((512 << lg)); n=$((bits / 16))
   run $bits:$n:3:16 "ticket" A=1
   run $bits:$n:3:16 "claims" BC_ORDERED_TICKET=0
 done
-run 5 "one-array chunk=786432" BC_ORDERED_CHUNK=786432
-run 5 "one-array chunk=393216" BC_ORDERED_CHUNK=393216
