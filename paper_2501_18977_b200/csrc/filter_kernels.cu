@@ -1646,6 +1646,9 @@ static cudaError_t launch_window(const KParams &p, u64 *words, const Src *src, c
     size_t smem = 0;
     for (int it = 0;; ++it) {
         cap = (u32)((chunk + ctas - 1) / ctas);
+        // whole tiles, the same number for each of the CTA's warps: a list
+        // of 257 entries would cost a ninth tile per round for one key
+        if (one && cap >= 128) cap = std::max(256u, (cap + 128u) & ~255u);
         smem = (size_t)cap * 24;
         // static + dynamic shared memory above 48 KB needs the opt-in
         if (cudaFuncSetAttribute(fw, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
