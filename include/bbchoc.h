@@ -187,6 +187,30 @@ BC_API int bc_format_answers(const uint64_t *h_keys, const uint8_t *h_answers, u
 BC_API int bc_parse_keys_text(const char *h_text, uint64_t len, uint64_t *h_keys, uint64_t cap,
                               uint64_t *consumed, uint64_t *lines, uint64_t *n_keys);
 
+/* Host-side FASTA ingestion (read_keys(..., "fasta"), io.py:226-242 _read_fasta,
+ * and the CLI's build from FASTA): joins the sequence lines of every record of
+ * h_text[0, len) -- lines split at '\n', stripped of surrounding ASCII
+ * whitespace, blank lines skipped, a line starting with '>' closing the record
+ * in progress -- into h_out, consecutive records separated by one `sep` byte (a
+ * non-ACGT byte, so no q-gram window spans two records: the input of
+ * bc_insert_qgrams / bc_contains_qgrams).  Output is appended at
+ * h_out[out_len_in...]; the caller sizes h_out for out_len_in + len + 1 bytes.
+ * *state carries bit 0 "a header was seen" and bit 1 "the record at the end of
+ * h_out is still open" from call to call; h_out[0, out_len_in) is the output so
+ * far (closed records, then the open one's sequence if bit 1 is set; a call
+ * may also start from an empty buffer that holds only the carried open
+ * record).  rec_ends[i] = end
+ * offset in h_out of the i-th record closed by this call (at most rec_cap;
+ * the number of '>' bytes in the text plus one is enough).  Without at_eof,
+ * parsing stops after the last '\n' (*consumed bytes used; the caller carries
+ * the partial line); with it the last line needs no '\n' and an open record is
+ * closed.  Sequence before the first header is BC_EINVAL, as the reference's
+ * KeyFormatError. */
+BC_API int bc_fasta_join(const char *h_text, uint64_t len, int at_eof, uint8_t sep,
+                         uint32_t *state, uint8_t *h_out, uint64_t out_len_in,
+                         uint64_t *out_len, uint64_t *rec_ends, uint64_t rec_cap,
+                         uint64_t *n_recs, uint64_t *consumed);
+
 /* ---- multi-GPU replica merge over peer memory (distributed.py) ----------------
  * CUDA IPC mapping of a device buffer for the other ranks: the 64-byte handle
  * of the allocation holding d_ptr and d_ptr's offset in it (torch's caching

@@ -26,7 +26,7 @@ EXPORTS = (
     "bc_insert_host", "bc_contains_host", "bc_encode_qgrams", "bc_insert_qgrams",
     "bc_contains_qgrams", "bc_block_histogram", "bc_route", "bc_eval_hash",
     "bc_last_error", "bc_launch_count", "bc_version", "bc_pcg64_fill", "bc_l2_release",
-    "bc_format_answers", "bc_parse_keys_text", "bc_ipc_export", "bc_ipc_import",
+    "bc_format_answers", "bc_parse_keys_text", "bc_fasta_join", "bc_ipc_export", "bc_ipc_import",
     "bc_ipc_close", "bc_peer_span", "bc_or_allreduce_peers", "bc_insert_peers",
 )
 
@@ -95,6 +95,7 @@ def lib() -> ctypes.CDLL:
         L.bc_l2_release.restype = None
         L.bc_format_answers.argtypes = [P, P, u64, P, u64, P]
         L.bc_parse_keys_text.argtypes = [P, u64, P, u64, P, P, P]
+        L.bc_fasta_join.argtypes = [P, u64, ci, ctypes.c_uint8, P, P, u64, P, P, u64, P, P]
         L.bc_ipc_export.argtypes = [P, P, P]
         L.bc_ipc_import.argtypes = [P, u64, P]
         L.bc_ipc_close.argtypes = [P, u64]
@@ -107,7 +108,7 @@ def lib() -> ctypes.CDLL:
                     "bc_filter_create", "bc_insert", "bc_contains", "bc_insert_host",
                     "bc_contains_host", "bc_encode_qgrams", "bc_insert_qgrams",
                     "bc_contains_qgrams", "bc_block_histogram", "bc_route", "bc_eval_hash",
-                    "bc_pcg64_fill", "bc_format_answers", "bc_parse_keys_text",
+                    "bc_pcg64_fill", "bc_format_answers", "bc_parse_keys_text", "bc_fasta_join",
                     "bc_ipc_export", "bc_ipc_import", "bc_ipc_close", "bc_peer_span",
                     "bc_or_allreduce_peers", "bc_insert_peers"):
                 fn.restype = ctypes.c_int

@@ -859,6 +859,65 @@ extern "C" int bc_parse_keys_text(const char *h_text, uint64_t len, uint64_t *h_
     return BC_OK;
 }
 
+// FASTA lines -> records joined with a separator byte (reference io.py:226-242,
+// _read_fasta: lines stripped of surrounding whitespace, header lines close the
+// record in progress, blank lines skipped, sequence before the first header is
+// an error).  One memchr + memcpy per line.
+extern "C" int bc_fasta_join(const char *h_text, uint64_t len, int at_eof, uint8_t sep,
+                             uint32_t *state, uint8_t *h_out, uint64_t out_len_in,
+                             uint64_t *out_len, uint64_t *rec_ends, uint64_t rec_cap,
+                             uint64_t *n_recs, uint64_t *consumed) {
+    if (!state || !out_len || !n_recs || !consumed) return fail(BC_EINVAL, "null output");
+    if ((len && !h_text) || !h_out) return fail(BC_EINVAL, "null buffer");
+    bool seen = (*state & 1u) != 0, open = (*state & 2u) != 0;
+    const char *p = h_text, *end = h_text + len;
+    u64 o = out_len_in, nr = 0;
+    *out_len = o;
+    *n_recs = 0;
+    *consumed = 0;
+    // an open record carried in h_out[0, out_len_in) must hold at least one base
+    if (open && o == 0) return fail(BC_EINVAL, "open record without bytes");
+    while (p < end) {
+        const char *nl = static_cast<const char *>(std::memchr(p, '\n', (size_t)(end - p)));
+        if (!nl) {
+            if (!at_eof) break;  // partial line: the caller carries it
+            nl = end;
+        }
+        const char *b = p, *e = nl;
+        while (b < e && is_space(*b)) ++b;
+        while (e > b && is_space(e[-1])) --e;
+        if (b < e) {
+            if (*b == '>') {
+                if (open) {
+                    if (nr >= rec_cap) return fail(BC_EINVAL, "record table full");
+                    rec_ends[nr++] = o;
+                    open = false;
+                }
+                seen = true;
+            } else {
+                if (!seen) return fail(BC_EINVAL, "FASTA input does not start with a header line");
+                if (!open) {
+                    if (o) h_out[o++] = sep;  // between records only
+                    open = true;
+                }
+                std::memcpy(h_out + o, b, (size_t)(e - b));
+                o += (u64)(e - b);
+            }
+        }
+        p = nl < end ? nl + 1 : end;
+    }
+    if (at_eof && p == end && open) {
+        if (nr >= rec_cap) return fail(BC_EINVAL, "record table full");
+        rec_ends[nr++] = o;
+        open = false;
+    }
+    *state = (seen ? 1u : 0u) | (open ? 2u : 0u);
+    *out_len = o;
+    *n_recs = nr;
+    *consumed = (u64)(p - h_text);
+    return BC_OK;
+}
+
 // ---- parallel host copies -------------------------------------------------------------
 // Pageable caller buffers are staged through pinned memory with memcpy; one
 // thread copies ~14 GB/s, a quarter of the PCIe Gen5 link, so the copies of a

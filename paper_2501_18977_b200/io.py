@@ -240,22 +240,77 @@ def fasta_records(fh: BinaryIO) -> Iterator[bytes]:
         yield b"".join(parts)
 
 
+def _fasta_joined(fh: BinaryIO, read_bytes: int = 1 << 26):
+    """Records of a FASTA stream joined natively (bc_fasta_join: one memchr +
+    memcpy per line instead of a Python loop over lines).  Yields (buf, ends):
+    the records closed by one read, joined with b"\\n" in the uint8 array buf,
+    ends[i] = end offset of record i.  A record still open at the end of a read
+    is carried into the next one, so records are never split."""
+    lib = _native.lib()
+    state = ctypes.c_uint32(0)
+    counters = (ctypes.c_uint64 * 3)()  # out_len, n_recs, consumed
+    carry_text = b""
+    carry_rec = np.empty(0, dtype=np.uint8)
+
+    def join(ptr, n, eof, out, out_len, ends, n_ends):
+        rc = lib.bc_fasta_join(ptr, n, int(eof), 0x0A, ctypes.byref(state), out.ctypes.data,
+                               out_len, ctypes.byref(counters, 0),
+                               ends.ctypes.data + 8 * n_ends, ends.size - n_ends,
+                               ctypes.byref(counters, 8), ctypes.byref(counters, 16))
+        if rc != _native.BC_OK:
+            raise KeyFormatError(lib.bc_last_error().decode(errors="replace"))
+        return int(counters[0]), n_ends + int(counters[1]), int(counters[2])
+
+    while True:
+        data = fh.read(read_bytes)
+        eof = not data
+        ends = np.empty(carry_text.count(b">") + data.count(b">") + 2, dtype=np.uint64)
+        out = np.empty(carry_rec.size + len(carry_text) + len(data) + 2, dtype=np.uint8)
+        out[:carry_rec.size] = carry_rec
+        out_len, n = carry_rec.size, 0
+        # the line the last read cut in two, completed with the head of this one
+        # (only that line is copied; the rest of the read is parsed in place)
+        nl = data.find(b"\n")
+        if eof or nl < 0:
+            head, off = carry_text + data, len(data)
+        else:
+            head, off = carry_text + data[:nl + 1], nl + 1
+        out_len, n, used = join(head, len(head), eof, out, out_len, ends, n)
+        carry_text = head[used:]
+        if off < len(data):
+            view = np.frombuffer(data, dtype=np.uint8)
+            out_len, n, used = join(view.ctypes.data + off, len(data) - off, False, out,
+                                    out_len, ends, n)
+            carry_text = data[off + used:]
+        closed = int(ends[n - 1]) if n else 0
+        if state.value & 2:  # the last record goes on in the next read
+            start = closed + 1 if n else 0
+            carry_rec = out[start:out_len].copy()
+        else:
+            carry_rec = np.empty(0, dtype=np.uint8)
+        if n:
+            yield out[:closed], ends[:n]
+        if eof:
+            return
+
+
 def fasta_batches(path, batch_bytes: int = 1 << 28) -> Iterator[bytes]:
     """FASTA records joined (join_records) into batches of about batch_bytes,
     for the fused q-gram kernels: the windows of a batch are those of its
     records, in order, and none spans two records."""
     fh = _open_binary(path)
     try:
-        batch: list = []
-        size = 0
-        for rec in fasta_records(fh):
-            batch.append(rec)
-            size += len(rec) + 1
-            if size >= batch_bytes:
-                yield join_records(batch)
-                batch, size = [], 0
-        if batch:
-            yield join_records(batch)
+        for buf, ends in _fasta_joined(fh):
+            a = 0  # offset of the batch's first record
+            i = 0
+            while i < ends.size:
+                # first record whose end brings the batch to batch_bytes
+                # (each record counts its length plus one, as join_records would)
+                j = int(np.searchsorted(ends, a + batch_bytes - 1, side="left"))
+                j = min(max(j, i), ends.size - 1)
+                e = int(ends[j])
+                yield buf[a:e].tobytes()
+                a, i = e + 1, j + 1
     finally:
         if fh is not sys.stdin.buffer:
             fh.close()

@@ -149,6 +149,39 @@ def test_fasta_batches_keep_records_whole_and_in_order(tmp_path):
         list(fasta_batches(str(bad)))
 
 
+def test_native_fasta_join_equals_the_line_loop(tmp_path):
+    """bc_fasta_join (fasta_batches) against the reference's line loop
+    (fasta_records, io.py:226-242) on ragged inputs: CRLF, blank and
+    whitespace-only lines, indented lines, empty records, '>' inside a
+    sequence line, no newline at the end, a header as the last line; read in
+    chunks of a few bytes, so lines and records straddle every boundary."""
+    import io as pyio
+
+    from paper_2501_18977_b200.io import _fasta_joined, fasta_records
+
+    rng = np.random.default_rng(11)
+    pieces = [b">h\n", b">h desc > more\r\n", b"  >indented header\n", b"\n", b"  \t \r\n",
+              b"ACGT\n", b"acgtnN\r\n", b"  GGA  \n", b"AC>GT\n", b"T" * 300 + b"\n",
+              b"\x0b\x0cCA\x0c\n", b"A C\tG\n"]
+    for trial in range(60):
+        body = b">first\n" + b"".join(pieces[i] for i in rng.integers(0, len(pieces), 40))
+        tail = [b"", b"ACG", b">last", b"  "][trial % 4]
+        data = body + tail
+        want = list(fasta_records(pyio.BytesIO(data)))
+        for read_bytes in (1, 7, 64, 1 << 20):
+            got = []
+            for buf, ends in _fasta_joined(pyio.BytesIO(data), read_bytes=read_bytes):
+                a = 0
+                for e in ends:
+                    got.append(buf[a:int(e)].tobytes())
+                    a = int(e) + 1
+            assert got == want, (trial, read_bytes)
+    with pytest.raises(KeyFormatError, match="header"):
+        list(_fasta_joined(pyio.BytesIO(b"\n  \nACGT\n>h\nAC\n")))
+    assert list(_fasta_joined(pyio.BytesIO(b""))) == []
+    assert list(_fasta_joined(pyio.BytesIO(b">only a header"))) == []
+
+
 @pytest.mark.gpu
 def test_gpu_filter_roundtrip_and_fasta(tmp_path):
     from oracle import oracle as orc

@@ -208,6 +208,10 @@ def row_fasta(bb, torch, out, tmp):
     def parse_only():
         return sum(len(b) for b in bio.fasta_batches(p, batch_bytes=1 << 24))
 
+    def parse_python():  # the reference's line loop (io.py:226-242)
+        with open(p, "rb") as fh:
+            return sum(len(r) for r in bio.fasta_records(fh))
+
     batches = list(bio.fasta_batches(p, batch_bytes=1 << 24))
 
     def insert_only():
@@ -222,12 +226,14 @@ def row_fasta(bb, torch, out, tmp):
     t = wall(run)
     total = run()
     tp = wall(parse_only)
+    tpy = wall(parse_python)
     insert_only()
     ti = min(insert_only() for _ in range(3))
     out({"row": "fasta", "workload": f"{nrec} records x {rec_len} bp -> fused canonical 31-mer insert",
          "bases_s": round(nrec * rec_len / t, 1), "kmers": total,
          "kmers_expected": nrec * (rec_len - 30),
          "parse_bases_s": round(nrec * rec_len / tp, 1),
+         "cpu_reference_parse_bases_s": round(nrec * rec_len / tpy, 1),
          "insert_bases_s": round(nrec * rec_len / ti, 1),
          "file_bytes": os.path.getsize(p), "host_cores": os.cpu_count(),
          "parity": "identical" if total == nrec * (rec_len - 30) else "DIFF"})
