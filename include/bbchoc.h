@@ -200,8 +200,11 @@ BC_API int bc_parse_keys_text(const char *h_text, uint64_t len, uint64_t *h_keys
  * far (closed records, then the open one's sequence if bit 1 is set; a call
  * may also start from an empty buffer that holds only the carried open
  * record).  rec_ends[i] = end
- * offset in h_out of the i-th record closed by this call (at most rec_cap;
- * the number of '>' bytes in the text plus one is enough).  Without at_eof,
+ * offset in h_out of the i-th record closed by this call.  When the table is
+ * full (*n_recs == rec_cap) the call stops before the line that would close
+ * another record, state unchanged: call again from h_text + *consumed with more
+ * table space (at the end of the text too: with len 0 and at_eof, to close
+ * the last record).  Without at_eof,
  * parsing stops after the last '\n' (*consumed bytes used; the caller carries
  * the partial line); with it the last line needs no '\n' and an open record is
  * closed.  Sequence before the first header is BC_EINVAL, as the reference's

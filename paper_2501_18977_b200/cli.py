@@ -119,7 +119,7 @@ def cmd_build(args) -> int:
             raise KeyFormatError("FASTA input needs a q-gram length")
         enc = QGramEncoder(q=args.q, canonical=not args.no_canonical)
         filt = Filter.from_config(config.validated())
-        for batch in fasta_batches(args.keys):
+        for batch in fasta_batches(args.keys, as_array=True):
             filt.insert_qgrams(enc, batch)
     else:
         filt = build_sharded(config, _key_stream(args))

@@ -889,7 +889,7 @@ extern "C" int bc_fasta_join(const char *h_text, uint64_t len, int at_eof, uint8
         if (b < e) {
             if (*b == '>') {
                 if (open) {
-                    if (nr >= rec_cap) return fail(BC_EINVAL, "record table full");
+                    if (nr >= rec_cap) break;  // table full: this line is not consumed
                     rec_ends[nr++] = o;
                     open = false;
                 }
@@ -906,8 +906,7 @@ extern "C" int bc_fasta_join(const char *h_text, uint64_t len, int at_eof, uint8
         }
         p = nl < end ? nl + 1 : end;
     }
-    if (at_eof && p == end && open) {
-        if (nr >= rec_cap) return fail(BC_EINVAL, "record table full");
+    if (at_eof && p == end && open && nr < rec_cap) {
         rec_ends[nr++] = o;
         open = false;
     }

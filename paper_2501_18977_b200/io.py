@@ -252,19 +252,30 @@ def _fasta_joined(fh: BinaryIO, read_bytes: int = 1 << 26):
     carry_text = b""
     carry_rec = np.empty(0, dtype=np.uint8)
 
-    def join(ptr, n, eof, out, out_len, ends, n_ends):
-        rc = lib.bc_fasta_join(ptr, n, int(eof), 0x0A, ctypes.byref(state), out.ctypes.data,
-                               out_len, ctypes.byref(counters, 0),
-                               ends.ctypes.data + 8 * n_ends, ends.size - n_ends,
-                               ctypes.byref(counters, 8), ctypes.byref(counters, 16))
-        if rc != _native.BC_OK:
-            raise KeyFormatError(lib.bc_last_error().decode(errors="replace"))
-        return int(counters[0]), n_ends + int(counters[1]), int(counters[2])
+    def join(buf, off, eof, out, out_len, ends, n_ends):
+        """Parse buf[off:] (bytes); returns (out_len, ends, n_ends, bytes used)."""
+        view = np.frombuffer(buf, dtype=np.uint8)
+        used = 0
+        while True:
+            rc = lib.bc_fasta_join(view.ctypes.data + off + used, len(buf) - off - used,
+                                   int(eof), 0x0A, ctypes.byref(state), out.ctypes.data,
+                                   out_len, ctypes.byref(counters, 0),
+                                   ends.ctypes.data + 8 * n_ends, ends.size - n_ends,
+                                   ctypes.byref(counters, 8), ctypes.byref(counters, 16))
+            if rc != _native.BC_OK:
+                raise KeyFormatError(lib.bc_last_error().decode(errors="replace"))
+            out_len = int(counters[0])
+            n_ends += int(counters[1])
+            used += int(counters[2])
+            if n_ends < ends.size:
+                return out_len, ends, n_ends, used
+            # record table full: more space, and on from the line it stopped at
+            ends = np.concatenate([ends, np.empty(max(1024, ends.size), dtype=np.uint64)])
 
     while True:
         data = fh.read(read_bytes)
         eof = not data
-        ends = np.empty(carry_text.count(b">") + data.count(b">") + 2, dtype=np.uint64)
+        ends = np.empty(1024 + len(data) // 4096, dtype=np.uint64)
         out = np.empty(carry_rec.size + len(carry_text) + len(data) + 2, dtype=np.uint8)
         out[:carry_rec.size] = carry_rec
         out_len, n = carry_rec.size, 0
@@ -275,12 +286,10 @@ def _fasta_joined(fh: BinaryIO, read_bytes: int = 1 << 26):
             head, off = carry_text + data, len(data)
         else:
             head, off = carry_text + data[:nl + 1], nl + 1
-        out_len, n, used = join(head, len(head), eof, out, out_len, ends, n)
+        out_len, ends, n, used = join(head, 0, eof, out, out_len, ends, n)
         carry_text = head[used:]
         if off < len(data):
-            view = np.frombuffer(data, dtype=np.uint8)
-            out_len, n, used = join(view.ctypes.data + off, len(data) - off, False, out,
-                                    out_len, ends, n)
+            out_len, ends, n, used = join(data, off, False, out, out_len, ends, n)
             carry_text = data[off + used:]
         closed = int(ends[n - 1]) if n else 0
         if state.value & 2:  # the last record goes on in the next read
@@ -294,10 +303,11 @@ def _fasta_joined(fh: BinaryIO, read_bytes: int = 1 << 26):
             return
 
 
-def fasta_batches(path, batch_bytes: int = 1 << 28) -> Iterator[bytes]:
+def fasta_batches(path, batch_bytes: int = 1 << 28, as_array: bool = False) -> Iterator[bytes]:
     """FASTA records joined (join_records) into batches of about batch_bytes,
     for the fused q-gram kernels: the windows of a batch are those of its
-    records, in order, and none spans two records."""
+    records, in order, and none spans two records.  as_array: yield uint8
+    views of the parser's buffer instead of bytes copies."""
     fh = _open_binary(path)
     try:
         for buf, ends in _fasta_joined(fh):
@@ -309,7 +319,7 @@ def fasta_batches(path, batch_bytes: int = 1 << 28) -> Iterator[bytes]:
                 j = int(np.searchsorted(ends, a + batch_bytes - 1, side="left"))
                 j = min(max(j, i), ends.size - 1)
                 e = int(ends[j])
-                yield buf[a:e].tobytes()
+                yield buf[a:e] if as_array else buf[a:e].tobytes()
                 a, i = e + 1, j + 1
     finally:
         if fh is not sys.stdin.buffer:

@@ -176,6 +176,22 @@ def test_native_fasta_join_equals_the_line_loop(tmp_path):
                     got.append(buf[a:int(e)].tobytes())
                     a = int(e) + 1
             assert got == want, (trial, read_bytes)
+    # more records than the parser's first record table holds (it stops at the
+    # line that needs a slot and is called again with a larger table)
+    many = b"".join(b">r%d\nAC\nG%s\n" % (i, b"T" * (i % 5)) for i in range(7000)) + b">x\nA"
+    want = list(fasta_records(pyio.BytesIO(many)))
+    got = []
+    for buf, ends in _fasta_joined(pyio.BytesIO(many)):
+        a = 0
+        for e in ends:
+            got.append(buf[a:int(e)].tobytes())
+            a = int(e) + 1
+    assert got == want and len(got) == 7001
+    from paper_2501_18977_b200.io import fasta_batches
+    fa = tmp_path / "many.fa"
+    fa.write_bytes(many)
+    arr = list(fasta_batches(str(fa), batch_bytes=1000, as_array=True))
+    assert b"\n".join(a.tobytes() for a in arr) == bb.join_records(want)
     with pytest.raises(KeyFormatError, match="header"):
         list(_fasta_joined(pyio.BytesIO(b"\n  \nACGT\n>h\nAC\n")))
     assert list(_fasta_joined(pyio.BytesIO(b""))) == []

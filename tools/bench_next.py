@@ -200,19 +200,19 @@ def row_fasta(bb, torch, out, tmp):
     def run():
         f = bb.Filter.from_config(cfg, insert_mode="relaxed")
         total = 0
-        for batch in bio.fasta_batches(p, batch_bytes=1 << 24):
+        for batch in bio.fasta_batches(p, batch_bytes=1 << 24, as_array=True):
             total += f.insert_qgrams(enc, batch)
         torch.cuda.synchronize()
         return total
 
     def parse_only():
-        return sum(len(b) for b in bio.fasta_batches(p, batch_bytes=1 << 24))
+        return sum(len(b) for b in bio.fasta_batches(p, batch_bytes=1 << 24, as_array=True))
 
     def parse_python():  # the reference's line loop (io.py:226-242)
         with open(p, "rb") as fh:
             return sum(len(r) for r in bio.fasta_records(fh))
 
-    batches = list(bio.fasta_batches(p, batch_bytes=1 << 24))
+    batches = list(bio.fasta_batches(p, batch_bytes=1 << 24, as_array=True))
 
     def insert_only():
         f = bb.Filter.from_config(cfg, insert_mode="relaxed")
