@@ -70,9 +70,38 @@ def write_filter(filt: Filter, path) -> None:
             fh.write(np.ascontiguousarray(st.words_readonly(), dtype="<u8").tobytes())
             return
         d = st.d_words
-        for a in range(0, st.num_words, _SLICE_WORDS):
+        if sys.byteorder != "little":
+            for a in range(0, st.num_words, _SLICE_WORDS):
+                b = min(st.num_words, a + _SLICE_WORDS)
+                fh.write(d[a:b].cpu().numpy().astype("<u8", copy=False).tobytes())
+            return
+        # two pinned slices: the device->host copy of slice i runs under the
+        # file write of slice i - 1, and the file is written from the pinned
+        # buffer itself (no bytes copies)
+        import torch
+
+        pins, evs = _pinned_slices(min(st.num_words, _SLICE_WORDS))
+        prev = None  # (buffer index, words)
+        for i, a in enumerate(range(0, st.num_words, _SLICE_WORDS)):
             b = min(st.num_words, a + _SLICE_WORDS)
-            fh.write(d[a:b].cpu().numpy().astype("<u8", copy=False).tobytes())
+            pins[i % 2][:b - a].copy_(d[a:b].view(torch.int64), non_blocking=True)
+            evs[i % 2].record()
+            if prev is not None:
+                evs[prev[0]].synchronize()
+                fh.write(memoryview(pins[prev[0]].numpy())[:prev[1]])
+            prev = (i % 2, b - a)
+        if prev is not None:
+            evs[prev[0]].synchronize()
+            fh.write(memoryview(pins[prev[0]].numpy())[:prev[1]])
+
+
+def _pinned_slices(nwords: int):
+    """Two page-locked int64 buffers of nwords and an event for each."""
+    import torch
+
+    pins = [torch.empty(nwords, dtype=torch.int64, pin_memory=True) for _ in range(2)]
+    evs = [torch.cuda.Event() for _ in range(2)]
+    return pins, evs
 
 
 def _check_header(fields) -> tuple:
@@ -120,17 +149,39 @@ def read_filter(path, **kw) -> Filter:
         on_device = torch.cuda.is_available()
         host = None if on_device else np.empty(st.num_words, dtype=np.uint64)
         got = 0
-        for a in range(0, st.num_words, _SLICE_WORDS):
-            b = min(st.num_words, a + _SLICE_WORDS)
-            chunk = fh.read((b - a) * 8)
-            got += len(chunk)
-            if len(chunk) != (b - a) * 8:
-                raise FilterFormatError(f"bit array has {got} bytes, expected {nbytes}")
-            words = np.frombuffer(chunk, dtype="<u8").astype(np.uint64)
-            if on_device:
-                st.d_words[a:b].copy_(torch.from_numpy(words))
-            else:
-                host[a:b] = words
+        if on_device and sys.byteorder == "little":
+            # the file is read straight into two pinned slices; the host->device
+            # copy of slice i runs under the read of slice i + 1
+            pins, evs = _pinned_slices(min(st.num_words, _SLICE_WORDS))
+            dw = st.d_words.view(torch.int64)
+            for i, a in enumerate(range(0, st.num_words, _SLICE_WORDS)):
+                b = min(st.num_words, a + _SLICE_WORDS)
+                evs[i % 2].synchronize()  # its last copy out of this buffer is done
+                view = memoryview(pins[i % 2].numpy()).cast("B")[:(b - a) * 8]
+                n = 0
+                while n < len(view):  # short reads (pipes) are topped up
+                    r = fh.readinto(view[n:])
+                    if not r:
+                        break
+                    n += r
+                got += n
+                if n != (b - a) * 8:
+                    raise FilterFormatError(f"bit array has {got} bytes, expected {nbytes}")
+                dw[a:b].copy_(pins[i % 2][:b - a], non_blocking=True)
+                evs[i % 2].record()
+            torch.cuda.current_stream().synchronize()
+        else:
+            for a in range(0, st.num_words, _SLICE_WORDS):
+                b = min(st.num_words, a + _SLICE_WORDS)
+                chunk = fh.read((b - a) * 8)
+                got += len(chunk)
+                if len(chunk) != (b - a) * 8:
+                    raise FilterFormatError(f"bit array has {got} bytes, expected {nbytes}")
+                words = np.frombuffer(chunk, dtype="<u8").astype(np.uint64)
+                if on_device:
+                    st.d_words[a:b].copy_(torch.from_numpy(words))
+                else:
+                    host[a:b] = words
         if fh.read(1):
             raise FilterFormatError(f"bit array has more than {nbytes} bytes, expected {nbytes}")
     if on_device:

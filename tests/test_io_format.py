@@ -232,6 +232,34 @@ def test_gpu_filter_roundtrip_and_fasta(tmp_path):
     np.testing.assert_array_equal(chunks[1], orc.encode_qgrams(b"NNACGTAAAC", 5))
 
 
+@pytest.mark.gpu
+def test_gpu_filter_files_in_many_slices(tmp_path, monkeypatch):
+    """Device filters are written and read through two pinned slices, the
+    copies overlapped with the file I/O: with slices of 777 words (several per
+    file, a ragged last one) the file equals the one written from the host
+    copy, reads give back the words, and a truncated file is still rejected."""
+    from paper_2501_18977_b200 import io as bio
+
+    cfg = bb.FilterConfig(kind="blowchoc", k=9, n_capacity=50_000, choices=2, seed=6)
+    f = bb.Filter.from_config(cfg)
+    f.insert_many(torch_keys := bb.even_keys(50_000, 3, device="cuda"))
+    want_words = f.storage.d_words.cpu().numpy().copy()
+    monkeypatch.setattr(bio, "_SLICE_WORDS", 777)
+    p = tmp_path / "sliced.bwch"
+    write_filter(f, p)                      # device words, pinned slices
+    raw = p.read_bytes()
+    assert raw[64:] == want_words.astype("<u8").tobytes()
+    g = read_filter(p)
+    np.testing.assert_array_equal(g.storage.d_words.cpu().numpy(), want_words)
+    assert g.contains_many(torch_keys).all()
+    (tmp_path / "cut.bwch").write_bytes(raw[:-5])
+    with pytest.raises(FilterFormatError, match="expected"):
+        read_filter(tmp_path / "cut.bwch")
+    (tmp_path / "long.bwch").write_bytes(raw + b"x")
+    with pytest.raises(FilterFormatError, match="more than"):
+        read_filter(tmp_path / "long.bwch")
+
+
 def _python_keys(text: bytes):
     """The reference's text rule (io.py:206-223) restated in Python."""
     keys = []
