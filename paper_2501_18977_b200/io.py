@@ -200,20 +200,44 @@ def _open_binary(path) -> BinaryIO:
 def _read_u64le(fh: BinaryIO, chunk: int) -> Iterator[np.ndarray]:
     """Raw little-endian records; short reads (pipes) are topped up, and a
     stream whose length is not a multiple of 8 is an error (io.py:191-203)."""
-    buf = bytearray()
-    want = chunk * 8
+    if sys.byteorder != "little" or not hasattr(fh, "readinto"):
+        buf = bytearray()
+        want = chunk * 8
+        while True:
+            got = fh.read(want - len(buf))
+            if got:
+                buf += got
+            if len(buf) >= want or (not got and len(buf) >= 8):
+                whole = len(buf) - len(buf) % 8
+                yield np.frombuffer(bytes(buf[:whole]), dtype="<u8").astype(np.uint64)
+                del buf[:whole]
+            if not got:
+                break
+        if buf:
+            raise KeyFormatError(f"u64le stream truncated ({len(buf)} stray bytes)")
+        return
+    # read straight into each chunk's array (no bytes objects in between)
+    stray = b""
     while True:
-        got = fh.read(want - len(buf))
-        if got:
-            buf += got
-        if len(buf) >= want or (not got and len(buf) >= 8):
-            whole = len(buf) - len(buf) % 8
-            yield np.frombuffer(bytes(buf[:whole]), dtype="<u8").astype(np.uint64)
-            del buf[:whole]
-        if not got:
+        arr = np.empty(chunk, dtype=np.uint64)
+        view = memoryview(arr).cast("B")
+        view[:len(stray)] = stray
+        n = len(stray)
+        eof = False
+        while n < len(view):
+            r = fh.readinto(view[n:])
+            if not r:
+                eof = True
+                break
+            n += r
+        whole = n - n % 8
+        stray = bytes(view[whole:n])
+        if whole:
+            yield arr[:whole // 8]
+        if eof:
             break
-    if buf:
-        raise KeyFormatError(f"u64le stream truncated ({len(buf)} stray bytes)")
+    if stray:
+        raise KeyFormatError(f"u64le stream truncated ({len(stray)} stray bytes)")
 
 
 _TEXT_BLOCK = 1 << 24  # bytes per native parse call
