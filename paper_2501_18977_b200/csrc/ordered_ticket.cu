@@ -440,7 +440,11 @@ bool ordered_ticket_supported(const KParams &p) {
     // c = 2: 2^18 blocks 3 812 / 3 167, 3*2^17 4 078 / 4 013, 2^19 4 007 / 4 921;
     // c = 3: 3*2^17 2 242 / 1 431, 2^19 ~1 850 (erratic: 290 .. 1 850) / 2 000,
     // 3*2^18 2 152 / 2 575
-    const u64 dflt = p.c >= 3 ? (1ull << 19) - 1 : (3ull << 17);
+    // Above 3*2^17 blocks the dataflow's rate is erratic for c = 3
+    // (tools/r2_ticket_stability.sh: 7*2^16 blocks 1 092 .. 1 980 Mkeys/s over
+    // four runs, 2^19 blocks 290 .. 1 851 over three sessions; steady at and
+    // below 3*2^17), so both limits sit there.
+    const u64 dflt = 3ull << 17;
     return p.num_blocks <= env_u64("BC_TICKET_MAX_BLOCKS", dflt);
 }
 

@@ -206,12 +206,12 @@ def test_cfg3_properties_full_size():
     ("cfg3", 3, 16, 16 * 2**28, 2**23),
     # config 5 geometry: 8 GiB, M = 2^27 blocks hashed onto 2^23 claim slots
     ("cfg5", 2, 11, 2**36, 2**22),
-    # the ticket dataflow's largest defaults: 3 * 2^17 blocks (c = 2), 2^19 - 1 (c = 3)
+    # the ticket dataflow's largest default: 3 * 2^17 blocks
     ("ticket_max_c2", 2, 14, 3 * 2**26, 2**23),
-    ("ticket_max_c3", 3, 16, 512 * (2**19 - 1), 2**23),
+    ("ticket_max_c3", 3, 16, 3 * 2**26, 2**23),
     # the smallest filters on the claim rounds: identity claim slots, window M / (2 c^2)
     ("claims_min_c2", 2, 14, 512 * (3 * 2**17 + 1), 2**23),
-    ("claims_min_c3", 3, 16, 2**28, 2**23),
+    ("claims_min_c3", 3, 16, 512 * (3 * 2**17 + 1), 2**23),
     ("claims_2p21_c3", 3, 16, 2**30, 2**23),
 ])
 def test_exact_order_full_geometry_matches_oracle(name, c, k, size_bits, n):
