@@ -315,7 +315,7 @@ def fasta_records(fh: BinaryIO) -> Iterator[bytes]:
         yield b"".join(parts)
 
 
-def _fasta_joined(fh: BinaryIO, read_bytes: int = 1 << 26):
+def _fasta_joined(fh: BinaryIO, read_bytes: int = 1 << 24):
     """Records of a FASTA stream joined natively (bc_fasta_join: one memchr +
     memcpy per line instead of a Python loop over lines).  Yields (buf, ends):
     the records closed by one read, joined with b"\\n" in the uint8 array buf,
@@ -378,13 +378,66 @@ def _fasta_joined(fh: BinaryIO, read_bytes: int = 1 << 26):
             return
 
 
-def fasta_batches(path, batch_bytes: int = 1 << 28, as_array: bool = False) -> Iterator[bytes]:
+def _prefetched(gen, depth: int):
+    """Run a generator in a background thread, `depth` items ahead of the
+    consumer (file reads and bc_fasta_join release the GIL, so parsing the
+    next batch overlaps the consumer's copy and insert of this one).  Returns
+    (iterator, stop): stop() ends the thread before the caller closes what
+    the generator reads from."""
+    import queue
+    import threading
+
+    q: queue.Queue = queue.Queue(maxsize=depth)
+    halt = threading.Event()
+    end = object()
+
+    def put(item) -> bool:
+        while not halt.is_set():
+            try:
+                q.put(item, timeout=0.05)
+                return True
+            except queue.Full:
+                continue
+        return False
+
+    def work():
+        try:
+            for item in gen:
+                if not put(item):
+                    return
+            put(end)
+        except BaseException as exc:  # handed to the consumer
+            put(exc)
+
+    thread = threading.Thread(target=work, name="fasta-prefetch", daemon=True)
+    thread.start()
+
+    def items():
+        while True:
+            item = q.get()
+            if item is end:
+                return
+            if isinstance(item, BaseException):
+                raise item
+            yield item
+
+    def stop():
+        halt.set()
+        thread.join()
+
+    return items(), stop
+
+
+def fasta_batches(path, batch_bytes: int = 1 << 28, as_array: bool = False,
+                  prefetch: int = 2) -> Iterator[bytes]:
     """FASTA records joined (join_records) into batches of about batch_bytes,
     for the fused q-gram kernels: the windows of a batch are those of its
     records, in order, and none spans two records.  as_array: yield uint8
-    views of the parser's buffer instead of bytes copies."""
+    views of the parser's buffer instead of bytes copies.  prefetch: batches
+    parsed ahead in a background thread (0: parse in the caller's thread)."""
     fh = _open_binary(path)
-    try:
+
+    def batches():
         for buf, ends in _fasta_joined(fh):
             a = 0  # offset of the batch's first record
             i = 0
@@ -396,7 +449,17 @@ def fasta_batches(path, batch_bytes: int = 1 << 28, as_array: bool = False) -> I
                 e = int(ends[j])
                 yield buf[a:e] if as_array else buf[a:e].tobytes()
                 a, i = e + 1, j + 1
+
+    stop = None
+    try:
+        if prefetch > 0:
+            it, stop = _prefetched(batches(), prefetch)
+            yield from it
+        else:
+            yield from batches()
     finally:
+        if stop is not None:
+            stop()
         if fh is not sys.stdin.buffer:
             fh.close()
 
