@@ -429,12 +429,17 @@ def _prefetched(gen, depth: int):
 
 
 def fasta_batches(path, batch_bytes: int = 1 << 28, as_array: bool = False,
-                  prefetch: int = 2) -> Iterator[bytes]:
+                  prefetch: int = 0) -> Iterator[bytes]:
     """FASTA records joined (join_records) into batches of about batch_bytes,
     for the fused q-gram kernels: the windows of a batch are those of its
     records, in order, and none spans two records.  as_array: yield uint8
     views of the parser's buffer instead of bytes copies.  prefetch: batches
-    parsed ahead in a background thread (0: parse in the caller's thread)."""
+    parsed ahead in a background thread (0, the default: parse in the caller's
+    thread).  Measured on the B200 box with the fused insert as consumer
+    (tools/fasta_prefetch_probe.py): 2 000 Mbp/s against 1 170-1 350 serial in
+    one process, but 1 969 / 709 / 582 over three runs of tools/bench_next.py
+    (bimodal, presumably where the parser thread's buffers land relative to
+    the GPU's host bridge), so it stays opt-in."""
     fh = _open_binary(path)
 
     def batches():

@@ -192,6 +192,14 @@ def test_native_fasta_join_equals_the_line_loop(tmp_path):
     fa.write_bytes(many)
     arr = list(fasta_batches(str(fa), batch_bytes=1000, as_array=True))
     assert b"\n".join(a.tobytes() for a in arr) == bb.join_records(want)
+    # parsed ahead in a background thread: same batches; closing early stops it
+    ahead = list(fasta_batches(str(fa), batch_bytes=1000, prefetch=3))
+    assert ahead == [a.tobytes() for a in arr]
+    g = fasta_batches(str(fa), batch_bytes=100, prefetch=2)
+    next(g)
+    g.close()
+    import threading
+    assert not [t for t in threading.enumerate() if t.name == "fasta-prefetch"]
     with pytest.raises(KeyFormatError, match="header"):
         list(_fasta_joined(pyio.BytesIO(b"\n  \nACGT\n>h\nAC\n")))
     assert list(_fasta_joined(pyio.BytesIO(b""))) == []
