@@ -824,6 +824,98 @@ bool parse_line(const char *b, const char *e, u64 *v) {
 }
 }  // namespace
 
+static int parse_keys_serial(const char *h_text, uint64_t len, uint64_t *h_keys, uint64_t cap,
+                             uint64_t *consumed, uint64_t *lines, uint64_t *n_keys);
+
+// Large blocks are parsed by several threads: the text is cut at line ends
+// into one segment per thread, a first pass counts each segment's lines and
+// keys (memchr + strip), a second parses every segment straight into its
+// place in h_keys.  Anything the serial parser would not run through to the
+// end of the block -- more keys than cap, a rejected line -- is left to it, so
+// the outputs and the error are the serial parser's in every case.
+// BC_PARSE_THREADS (default min(16, cores); 1 = serial).
+static bool parse_keys_parallel(const char *h_text, uint64_t len, uint64_t *h_keys, uint64_t cap,
+                                uint64_t *consumed, uint64_t *lines, uint64_t *n_keys) {
+    static const unsigned kThreads = [] {
+        if (const char *e = std::getenv("BC_PARSE_THREADS")) return (unsigned)std::max(1, std::atoi(e));
+        return std::min(16u, std::max(1u, std::thread::hardware_concurrency()));
+    }();
+    const u64 kMinSeg = 1ull << 20;
+    const unsigned T = (unsigned)std::min<u64>(kThreads, len / kMinSeg);
+    if (T < 2) return false;
+    // whole lines only: [0, stop) ends after the last '\n'
+    const char *last = static_cast<const char *>(memrchr(h_text, '\n', (size_t)len));
+    if (!last) return false;
+    const u64 stop = (u64)(last - h_text) + 1;
+    std::vector<u64> cut(T + 1, stop);
+    cut[0] = 0;
+    for (unsigned t = 1; t < T; ++t) {
+        const u64 at = std::max(cut[t - 1], stop * t / T);
+        const char *nl = at < stop ? static_cast<const char *>(
+                                         std::memchr(h_text + at, '\n', (size_t)(stop - at)))
+                                   : nullptr;
+        cut[t] = nl ? (u64)(nl - h_text) + 1 : stop;
+    }
+    std::vector<u64> nkeys(T, 0), nlines(T, 0);
+    auto each_line = [&](unsigned t, auto &&on_line) {
+        const char *p = h_text + cut[t], *end = h_text + cut[t + 1];
+        while (p < end) {
+            const char *nl = static_cast<const char *>(std::memchr(p, '\n', (size_t)(end - p)));
+            const char *b = p, *e = nl;
+            while (b < e && is_space(*b)) ++b;
+            while (e > b && is_space(e[-1])) --e;
+            if (!on_line(b, e)) return false;
+            p = nl + 1;
+        }
+        return true;
+    };
+    {
+        std::vector<std::thread> th;
+        for (unsigned t = 0; t < T; ++t)
+            th.emplace_back([&, t] {
+                u64 k = 0, l = 0;
+                each_line(t, [&](const char *b, const char *e) {
+                    k += b < e;
+                    ++l;
+                    return true;
+                });
+                nkeys[t] = k;
+                nlines[t] = l;
+            });
+        for (auto &x : th) x.join();
+    }
+    u64 total = 0, total_lines = 0;
+    std::vector<u64> at(T, 0);
+    for (unsigned t = 0; t < T; ++t) {
+        at[t] = total;
+        total += nkeys[t];
+        total_lines += nlines[t];
+    }
+    if (total > cap) return false;  // the serial parser stops at cap keys
+    std::atomic<bool> bad{false};
+    {
+        std::vector<std::thread> th;
+        for (unsigned t = 0; t < T; ++t)
+            th.emplace_back([&, t] {
+                u64 *out = h_keys + at[t];
+                const bool ok = each_line(t, [&](const char *b, const char *e) {
+                    if (b == e) return true;
+                    u64 v;
+                    if (!parse_line(b, e, &v)) return false;
+                    *out++ = v;
+                    return !bad.load(std::memory_order_relaxed);
+                });
+                if (!ok) bad.store(true, std::memory_order_relaxed);
+            });
+        for (auto &x : th) x.join();
+    }
+    if (bad.load()) return false;  // the serial parser words the error
+    *consumed = stop;
+    *lines = total_lines;
+    *n_keys = total;
+    return true;
+}
+
 extern "C" int bc_parse_keys_text(const char *h_text, uint64_t len, uint64_t *h_keys,
                                   uint64_t cap, uint64_t *consumed, uint64_t *lines,
                                   uint64_t *n_keys) {
@@ -831,6 +923,13 @@ extern "C" int bc_parse_keys_text(const char *h_text, uint64_t len, uint64_t *h_
     *consumed = *lines = *n_keys = 0;
     if (len && !h_text) return fail(BC_EINVAL, "null text");
     if (cap && !h_keys) return fail(BC_EINVAL, "null key buffer");
+    if (parse_keys_parallel(h_text, len, h_keys, cap, consumed, lines, n_keys)) return BC_OK;
+    *consumed = *lines = *n_keys = 0;
+    return parse_keys_serial(h_text, len, h_keys, cap, consumed, lines, n_keys);
+}
+
+static int parse_keys_serial(const char *h_text, uint64_t len, uint64_t *h_keys, uint64_t cap,
+                             uint64_t *consumed, uint64_t *lines, uint64_t *n_keys) {
     const char *p = h_text, *end = h_text + len;
     u64 n = 0, line = 0;
     while (p < end && n < cap) {

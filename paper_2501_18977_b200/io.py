@@ -263,37 +263,58 @@ def _read_text(fh: BinaryIO, chunk: int) -> Iterator[np.ndarray]:
     nkeys = ctypes.c_uint64()
     fill = 0
     lineno = 1  # number of the first line still to parse
-    tail = b""
+    # one reusable block: the unparsed tail of the last read moves to its front
+    # and the file is read in behind it (no bytes objects, no concatenation)
+    buf = bytearray(_TEXT_BLOCK + 4096)
+    ntail = 0
     eof = False
     while not eof:
-        data = fh.read(_TEXT_BLOCK)
-        eof = not data
-        text = tail + data
+        if ntail + _TEXT_BLOCK + 1 > len(buf):  # a line longer than the slack
+            buf.extend(bytes(ntail + _TEXT_BLOCK + 1 - len(buf)))
+        mv = memoryview(buf)
+        got = _readinto(fh, mv[ntail:ntail + _TEXT_BLOCK])
+        mv.release()
+        eof = got == 0
+        n = ntail + got
         if eof:
-            if not text:
+            if not n:
                 break
-            text += b"\n"  # the last line needs no newline
-        view = np.frombuffer(text, dtype=np.uint8)
+            buf[n:n + 1] = b"\n"  # the last line needs no newline
+            n += 1
+        view = np.frombuffer(buf, dtype=np.uint8)
         off = 0
-        while off < len(text):
-            rc = lib.bc_parse_keys_text(view.ctypes.data + off, len(text) - off,
+        while off < n:
+            rc = lib.bc_parse_keys_text(view.ctypes.data + off, n - off,
                                         out.ctypes.data + 8 * fill, chunk - fill,
                                         ctypes.byref(used), ctypes.byref(nlines),
                                         ctypes.byref(nkeys))
             fill += nkeys.value
             if rc != _native.BC_OK:
                 start = off + used.value
-                stop = text.find(b"\n", start)
-                raise _text_error(text[start:stop], lineno + nlines.value)
+                stop = buf.find(b"\n", start, n)
+                raise _text_error(bytes(buf[start:stop]), lineno + nlines.value)
             off += used.value
             lineno += nlines.value
             if fill < chunk:
                 break  # every whole line is parsed; a partial one may remain
             yield out.copy()
             fill = 0
-        tail = text[off:]
+        del view
+        ntail = n - off
+        buf[:ntail] = buf[off:n]
     if fill:
         yield out[:fill].copy()
+
+
+def _readinto(fh: BinaryIO, view) -> int:
+    """Fill view from fh (short reads of pipes topped up); bytes read."""
+    n = 0
+    while n < len(view):
+        r = fh.readinto(view[n:])
+        if not r:
+            break
+        n += r
+    return n
 
 
 def fasta_records(fh: BinaryIO) -> Iterator[bytes]:

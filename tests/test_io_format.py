@@ -311,6 +311,57 @@ def test_native_text_parser_matches_python_int(tmp_path, monkeypatch, block):
     assert got.tolist() == _python_keys(text)
 
 
+@pytest.mark.parametrize("threads", ["1", "5"])
+def test_native_text_parser_large_blocks(tmp_path, threads):
+    """Blocks of several MB are cut at line ends and parsed by several threads
+    (BC_PARSE_THREADS, read at first use, hence the subprocess): the keys
+    equal Python's int() of every non-blank line; output chunks smaller than a
+    block and a rejected line far into the file behave as with one thread
+    (the reference's line number and wording, io.py:206-223)."""
+    import subprocess
+    import sys
+
+    script = r"""
+import numpy as np, sys
+from paper_2501_18977_b200.io import read_keys, KeyFormatError
+rng = np.random.default_rng(3)
+vals = rng.integers(0, 2**64, size=400_000, dtype=np.uint64).tolist()
+forms = []
+for i, v in enumerate(vals):
+    s = str(v)
+    k = i % 9
+    if k == 1: s = "+" + s
+    elif k == 2: s = "00" + s
+    elif k == 3 and len(s) > 4: s = s[:3] + "_" + s[3:]
+    elif k == 4: s = "  " + s + " \r"
+    elif k == 5: s = s + "\n"
+    elif k == 6: s = s + "\n \t"
+    forms.append(s)
+text = ("\n".join(forms)).encode()
+path = sys.argv[1]
+open(path, "wb").write(text)
+want = [int(l) for l in text.split(b"\n") if l.strip()]
+for chunk in (1 << 20, 70_001):
+    got = np.concatenate(list(read_keys(path, "text", chunk_size=chunk)))
+    assert got.tolist() == want, chunk
+lines = text.split(b"\n")
+bad_at = len(lines) - 1000
+lines[bad_at] = b"12x4"
+open(path, "wb").write(b"\n".join(lines))
+try:
+    list(read_keys(path, "text"))
+    print("no error")
+except KeyFormatError as e:
+    print(str(e) == f"line {bad_at + 1}: not an integer: b'12x4'", len(text))
+"""
+    out = subprocess.run([sys.executable, "-c", script, str(tmp_path / "big.txt")],
+                         env=dict(os.environ, BC_PARSE_THREADS=threads), capture_output=True,
+                         text=True, cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    assert out.returncode == 0, out.stderr
+    ok, size = out.stdout.split()
+    assert ok == "True" and int(size) > 6_000_000
+
+
 @pytest.mark.parametrize("bad,msg", [
     (b"1__0", "line 3: not an integer"), (b"_1", "line 3: not an integer"),
     (b"1_", "line 3: not an integer"), (b"0x10", "line 3: not an integer"),
