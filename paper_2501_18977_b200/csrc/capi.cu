@@ -745,6 +745,88 @@ extern "C" int bc_pcg64_fill(uint64_t state_hi, uint64_t state_lo, uint64_t inc_
 }
 
 // ---- CLI query output -----------------------------------------------------------------
+namespace {
+// Threads for the host-side text work (query TSV formatting, key parsing):
+// BC_PARSE_THREADS, default min(16, cores); 1 = serial.
+unsigned host_text_threads() {
+    static const unsigned t = [] {
+        if (const char *e = std::getenv("BC_PARSE_THREADS")) return (unsigned)std::max(1, std::atoi(e));
+        return std::min(16u, std::max(1u, std::thread::hardware_concurrency()));
+    }();
+    return t;
+}
+
+const struct DigitPairs {
+    char d[200];
+    DigitPairs() {
+        for (int i = 0; i < 100; ++i) {
+            d[2 * i] = (char)('0' + i / 10);
+            d[2 * i + 1] = (char)('0' + i % 10);
+        }
+    }
+} g_pairs;
+
+// "<key>\t<0|1>\n" for keys [i0, i1) at o; returns the end.
+char *format_range(const uint64_t *keys, const uint8_t *ans, uint64_t i0, uint64_t i1, char *o) {
+    for (uint64_t i = i0; i < i1; ++i) {
+        uint64_t v = keys[i];
+        char buf[20];
+        int p = 20;
+        while (v >= 100) {
+            const unsigned r = (unsigned)(v % 100);
+            v /= 100;
+            p -= 2;
+            std::memcpy(buf + p, g_pairs.d + 2 * r, 2);
+        }
+        if (v >= 10) {
+            p -= 2;
+            std::memcpy(buf + p, g_pairs.d + 2 * v, 2);
+        } else {
+            buf[--p] = (char)('0' + v);
+        }
+        std::memcpy(o, buf + p, 20 - p);
+        o += 20 - p;
+        o[0] = '\t';
+        o[1] = ans[i] ? '1' : '0';
+        o[2] = '\n';
+        o += 3;
+    }
+    return o;
+}
+
+// bytes format_range writes for keys [i0, i1)
+uint64_t format_bytes(const uint64_t *keys, uint64_t i0, uint64_t i1) {
+    static const uint64_t p10[20] = {1ull,
+                                     10ull,
+                                     100ull,
+                                     1000ull,
+                                     10000ull,
+                                     100000ull,
+                                     1000000ull,
+                                     10000000ull,
+                                     100000000ull,
+                                     1000000000ull,
+                                     10000000000ull,
+                                     100000000000ull,
+                                     1000000000000ull,
+                                     10000000000000ull,
+                                     100000000000000ull,
+                                     1000000000000000ull,
+                                     10000000000000000ull,
+                                     100000000000000000ull,
+                                     1000000000000000000ull,
+                                     10000000000000000000ull};
+    uint64_t total = 0;
+    for (uint64_t i = i0; i < i1; ++i) {
+        const uint64_t v = keys[i];
+        // digits from the bit length (1233 / 4096 ~ log10 2), corrected by one compare
+        const unsigned t = ((64u - (unsigned)__builtin_clzll(v | 1)) * 1233u) >> 12;
+        total += t + ((v | 1) < p10[t] ? 0u : 1u) + 3u;
+    }
+    return total;
+}
+}  // namespace
+
 extern "C" int bc_format_answers(const uint64_t *h_keys, const uint8_t *h_answers, uint64_t n,
                                  char *h_out, uint64_t out_cap, uint64_t *written) {
     if (!written) return fail(BC_EINVAL, "null byte count");
@@ -752,40 +834,30 @@ extern "C" int bc_format_answers(const uint64_t *h_keys, const uint8_t *h_answer
     if (n == 0) return BC_OK;
     if (!h_keys || !h_answers || !h_out) return fail(BC_EINVAL, "null keys, answers or output");
     if (out_cap / 23 < n) return fail(BC_EINVAL, "output buffer below 23 bytes per key");
-    static const struct Pairs {
-        char d[200];
-        Pairs() {
-            for (int i = 0; i < 100; ++i) {
-                d[2 * i] = (char)('0' + i / 10);
-                d[2 * i + 1] = (char)('0' + i % 10);
-            }
-        }
-    } pairs;
-    char *o = h_out;
-    for (uint64_t i = 0; i < n; ++i) {
-        uint64_t v = h_keys[i];
-        char buf[20];
-        int p = 20;
-        while (v >= 100) {
-            const unsigned r = (unsigned)(v % 100);
-            v /= 100;
-            p -= 2;
-            std::memcpy(buf + p, pairs.d + 2 * r, 2);
-        }
-        if (v >= 10) {
-            p -= 2;
-            std::memcpy(buf + p, pairs.d + 2 * v, 2);
-        } else {
-            buf[--p] = (char)('0' + v);
-        }
-        std::memcpy(o, buf + p, 20 - p);
-        o += 20 - p;
-        o[0] = '\t';
-        o[1] = h_answers[i] ? '1' : '0';
-        o[2] = '\n';
-        o += 3;
+    // large batches: a length pass gives every thread's output offset, then
+    // each formats its keys straight into place
+    const unsigned T = (unsigned)std::min<uint64_t>(host_text_threads(), n >> 17);
+    if (T < 2) {
+        *written = (uint64_t)(format_range(h_keys, h_answers, 0, n, h_out) - h_out);
+        return BC_OK;
     }
-    *written = (uint64_t)(o - h_out);
+    std::vector<uint64_t> at(T + 1, 0);
+    {
+        std::vector<std::thread> th;
+        for (unsigned t = 0; t < T; ++t)
+            th.emplace_back([&, t] { at[t + 1] = format_bytes(h_keys, n * t / T, n * (t + 1) / T); });
+        for (auto &x : th) x.join();
+    }
+    for (unsigned t = 0; t < T; ++t) at[t + 1] += at[t];
+    {
+        std::vector<std::thread> th;
+        for (unsigned t = 0; t < T; ++t)
+            th.emplace_back([&, t] {
+                format_range(h_keys, h_answers, n * t / T, n * (t + 1) / T, h_out + at[t]);
+            });
+        for (auto &x : th) x.join();
+    }
+    *written = at[T];
     return BC_OK;
 }
 
@@ -836,12 +908,8 @@ static int parse_keys_serial(const char *h_text, uint64_t len, uint64_t *h_keys,
 // BC_PARSE_THREADS (default min(16, cores); 1 = serial).
 static bool parse_keys_parallel(const char *h_text, uint64_t len, uint64_t *h_keys, uint64_t cap,
                                 uint64_t *consumed, uint64_t *lines, uint64_t *n_keys) {
-    static const unsigned kThreads = [] {
-        if (const char *e = std::getenv("BC_PARSE_THREADS")) return (unsigned)std::max(1, std::atoi(e));
-        return std::min(16u, std::max(1u, std::thread::hardware_concurrency()));
-    }();
     const u64 kMinSeg = 1ull << 20;
-    const unsigned T = (unsigned)std::min<u64>(kThreads, len / kMinSeg);
+    const unsigned T = (unsigned)std::min<u64>(host_text_threads(), len / kMinSeg);
     if (T < 2) return false;
     // whole lines only: [0, stop) ends after the last '\n'
     const char *last = static_cast<const char *>(memrchr(h_text, '\n', (size_t)len));

@@ -41,6 +41,21 @@ def test_format_answers_matches_python_formatting():
         cli.format_answers(keys, ans[:-1])
 
 
+def test_format_answers_large_batches_in_threads():
+    """Batches of 2^18 keys and more are formatted by several threads (a
+    length pass fixes every thread's output offset): every digit count, the
+    powers of ten and their neighbours included, lands where the serial
+    formatter puts it."""
+    rng = np.random.default_rng(8)
+    n = (1 << 19) + 77
+    keys = rng.integers(0, 2**64, n, dtype=np.uint64)
+    keys[: n // 2] >>= rng.integers(0, 64, n // 2).astype(np.uint64)
+    edge = [0, 1, 9, 2**64 - 1] + [10**k for k in range(20)] + [10**k - 1 for k in range(1, 20)]
+    keys[rng.choice(n, len(edge), replace=False)] = np.array(edge, dtype=np.uint64)
+    ans = rng.integers(0, 2, n).astype(bool)
+    assert cli.format_answers(keys, ans) == expected_tsv(keys, ans)
+
+
 def test_usage_errors_exit_1():
     assert cli.main([]) == cli.EXIT_USAGE
     assert cli.main(["build", "--kind", "blowchoc"]) == cli.EXIT_USAGE
