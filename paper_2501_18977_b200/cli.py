@@ -119,8 +119,8 @@ def cmd_build(args) -> int:
             raise KeyFormatError("FASTA input needs a q-gram length")
         enc = QGramEncoder(q=args.q, canonical=not args.no_canonical)
         filt = Filter.from_config(config.validated())
-        for batch in fasta_batches(args.keys, as_array=True):
-            filt.insert_qgrams(enc, batch)
+        filt.insert_qgram_batches(enc, fasta_batches(args.keys, batch_bytes=1 << 24,
+                                                     as_array=True))
     else:
         filt = build_sharded(config, _key_stream(args))
     wall = time.perf_counter() - t0

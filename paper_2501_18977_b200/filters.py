@@ -477,6 +477,35 @@ class Filter:
         self.inserted += cnt
         return cnt
 
+    def insert_qgram_batches(self, enc, batches, mode: str | None = None) -> int:
+        """insert_qgrams over an iterable of sequences (e.g. io.fasta_batches)
+        without a host sync per batch: every batch's count stays on the device
+        and all are read once at the end, so the host prepares (reads, parses)
+        the next batch while the GPU inserts this one.  Returns the total."""
+        from ._device import as_device_bytes, ptr, sequence_records, stream_ptr
+
+        m = self._mode(mode)
+        dev = self.device
+        slots: list = []  # device count arrays, 1024 batches each
+        used = 0
+        with torch.cuda.device(dev):
+            for sequence in batches:
+                flat, rec = sequence_records(sequence, None)
+                seq = as_device_bytes(flat, dev)
+                n = seq.numel()
+                if used % 1024 == 0:
+                    slots.append(torch.zeros(1024, dtype=torch.int64, device=dev))
+                check(lib().bc_insert_qgrams(self.handle, ptr(self.storage.d_words),
+                                             ptr(seq) if n else None, n, enc.q,
+                                             int(enc.canonical), rec, m,
+                                             ptr(slots[-1]) + 8 * (used % 1024),
+                                             stream_ptr(dev)))
+                used += 1
+            cnt = sum(int(t.sum().item()) for t in slots)
+        self.storage.device_modified()
+        self.inserted += cnt
+        return cnt
+
     def _qgram_lookup(self, enc, sequence, record_len, want_answers: bool):
         from ._device import as_device_bytes, ptr, sequence_records, stream_ptr
 

@@ -935,3 +935,19 @@ def test_fused_exact_qgram_insert_across_a_long_invalid_run(env):
         "print(bool(np.array_equal(f.storage.words, o.words)), want.size)\n")
     ok, n = _run_with_env(script, BC_ORDERED_TICKET="0", **env).split()
     assert ok == "True" and int(n) == 40000 - 24 + 50000 - 24
+
+
+def test_insert_qgram_batches_equals_one_insert_per_batch():
+    """insert_qgram_batches (counts read once at the end) against
+    insert_qgrams per batch, exact order: same words, same total."""
+    rng = np.random.default_rng(17)
+    recs = [rng.choice(np.frombuffer(b"ACGTN", np.uint8), size=int(n), p=[0.245] * 4 + [0.02])
+            for n in rng.integers(10, 5000, 40)]
+    batches = [bb.join_records([r.tobytes() for r in recs[i:i + 7]]) for i in range(0, 40, 7)]
+    enc = bb.QGramEncoder(19, canonical=True)
+    cfg = bb.FilterConfig(kind="blowchoc", k=8, choices=2, n_capacity=120_000, seed=3)
+    a, b = bb.Filter.from_config(cfg), bb.Filter.from_config(cfg)
+    total = sum(a.insert_qgrams(enc, x) for x in batches)
+    assert b.insert_qgram_batches(enc, iter(batches)) == total == a.inserted == b.inserted
+    np.testing.assert_array_equal(a.storage.words, b.storage.words)
+    assert bb.Filter.from_config(cfg).insert_qgram_batches(enc, []) == 0

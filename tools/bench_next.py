@@ -197,11 +197,10 @@ def row_fasta(bb, torch, out, tmp):
     enc = bb.QGramEncoder(q=31, canonical=True)
     cfg = bb.FilterConfig(kind="blowchoc", k=14, choices=2, size_bits=14 * nrec * rec_len, seed=1)
 
-    def run():
+    def run():  # as the CLI's build does: no host sync per batch
         f = bb.Filter.from_config(cfg, insert_mode="relaxed")
-        total = 0
-        for batch in bio.fasta_batches(p, batch_bytes=1 << 24, as_array=True):
-            total += f.insert_qgrams(enc, batch)
+        total = f.insert_qgram_batches(enc, bio.fasta_batches(p, batch_bytes=1 << 24,
+                                                              as_array=True))
         torch.cuda.synchronize()
         return total
 
